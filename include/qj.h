@@ -1,0 +1,199 @@
+/*
+ * qj.h -- C ABI of the B200 state-vector gate-application library (libqj.so).
+ *
+ * What it computes: Schroedinger state-vector gate application, Eq. 1 of
+ * "Quantum simulation with just-in-time compilation" (PAPER.md:79-86,
+ * \label{eq:gateapplication}):
+ *
+ *     psi'(sigma_1..tau..sigma_n) = sum_{tau'} G(tau, tau') psi(sigma_1..tau'..sigma_n)
+ *
+ * applied IN PLACE ("custom operators perform in-place
+ * updates"), with the sparsity of Pauli / controlled gates exploited
+ * and specialised X / Z / SWAP operators,
+ * plus fSim / diagonal entry points and circuit execution named by the
+ * BASELINE.json north star, and Born-rule probabilities.
+ *
+ * Conventions (DESIGN.md readings):
+ *   R1  qubit q is bit (n-1-q) of the basis index (qubit 0 = most significant).
+ *   R3  gate matrices are row-major 2^k x 2^k; the first-listed target is the
+ *       most significant bit of the row/column index.  Targets may be listed in
+ *       any order.
+ *   R4  controls: the gate acts only where every control qubit is 1.
+ *   Data: amplitudes are interleaved (re, im); complex64 = 2 x float,
+ *       complex128 = 2 x double.  Host-side matrices / diagonals / fSim
+ *       parameters are interleaved complex values IN THE STATE'S DTYPE.
+ *
+ * Ownership: the caller owns the amplitude buffer (e.g. a torch tensor:
+ * contiguous, 16-byte aligned, >= 2^n_local elements, alive while the handle
+ * lives).  The library owns its scratch (reduction bins, staged gate programs)
+ * and frees it in qj_state_free.  Every host array passed in (targets,
+ * controls, matrices, gate lists) is copied or consumed before the call
+ * returns; the caller may free it immediately.
+ *
+ * Execution: all device work is enqueued on the handle's CUDA stream and is
+ * asynchronous w.r.t. the host; qj_sync blocks.  A handle is not thread-safe:
+ * one thread mutates it at a time.
+ *
+ * Errors: every entry point returns a qj_status.  Argument errors are detected
+ * synchronously, before anything is enqueued, and leave the state untouched.
+ * Asynchronous CUDA failures surface as QJ_ERR_CUDA on a later call or on
+ * qj_sync.  qj_last_error() returns a thread-local message for the last failure.
+ * No C++ exception crosses this ABI.  Matrices are not checked for unitarity
+ * and the state is never renormalised.
+ */
+#ifndef QJ_H
+#define QJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    QJ_OK = 0,
+    QJ_ERR_INVALID_ARG = 1,        /* NULL pointer, nt < 1, n != state's n, bad flag */
+    QJ_ERR_INDEX_OUT_OF_RANGE = 2, /* qubit >= n, basis_index >= 2^n */
+    QJ_ERR_OVERLAPPING_QUBITS = 3, /* duplicate qubit, or targets and controls intersect */
+    QJ_ERR_TOO_MANY_TARGETS = 4,   /* nt > QJ_MAX_TARGETS or nc > QJ_MAX_CONTROLS */
+    QJ_ERR_CAPACITY = 5,           /* n outside [1, QJ_MAX_QUBITS] or shard too large */
+    QJ_ERR_DTYPE = 6,              /* unknown dtype */
+    QJ_ERR_CUDA = 7,               /* a CUDA runtime error (launch or asynchronous) */
+    QJ_ERR_NCCL = 8,               /* a NCCL error in the multi-GPU layer */
+    QJ_ERR_UNSUPPORTED = 9         /* valid request this build does not implement */
+} qj_status;
+
+typedef enum { QJ_C64 = 0, QJ_C128 = 1 } qj_dtype;
+
+typedef struct qj_state_s* qj_state;
+
+#define QJ_KEEP UINT64_MAX   /* qj_state_init: leave the buffer's contents as they are */
+#define QJ_MAX_TARGETS 8
+#define QJ_MAX_CONTROLS 16
+#define QJ_MAX_QUBITS 40     /* total qubits; a shard must also fit one GPU */
+
+/* ---- state handle ---------------------------------------------------------
+ * qj_state_init: wrap the caller's device buffer `amps_dev` (2^n amplitudes of
+ * dtype `dt` on the current device) and, unless basis_index == QJ_KEEP, write
+ * the basis state |basis_index> into it (|0..0> for 0).
+ * `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ * `nccl_comm` must be NULL in this build for a single-GPU state (see
+ * qj_state_init_sharded for sharded states).
+ * Errors: INVALID_ARG (out or amps_dev NULL), CAPACITY (n < 1 or n > 40),
+ * DTYPE, INDEX_OUT_OF_RANGE (basis_index >= 2^n), CUDA. */
+qj_status qj_state_init(qj_state* out, void* amps_dev, int n, qj_dtype dt,
+                        uint64_t basis_index, void* cuda_stream, void* nccl_comm);
+
+/* Sharded state on the top g = log2(nshards) "global" qubits (
+ * the paper's multi-device scheme is PAPER.md:469-489).  Shard r holds the
+ * 2^(n-g) amplitudes whose global bits equal r, while the qubit map is
+ * canonical.  `shards` = nshards device pointers, all owned by this process
+ * on this device (virtual ranks; nshards a power of two >= 1).  Gates on
+ * global qubits are applied through local<->global qubit swaps executed as
+ * device-to-device exchanges; qubit labels stay logical at this ABI. */
+qj_status qj_state_init_sharded(qj_state* out, void* const* shards, int nshards, int n,
+                                qj_dtype dt, uint64_t basis_index, void* cuda_stream);
+
+/* Re-initialise an existing handle to |basis_index> (QJ_KEEP: no-op). */
+qj_status qj_state_reset(qj_state s, uint64_t basis_index);
+
+/* Release the handle and library scratch.  The amplitude buffer is the caller's. */
+qj_status qj_state_free(qj_state s);
+
+/* ---- gate application (Eq. 1) ----------------------------------------------
+ * qj_apply_gate: apply the 2^nt x 2^nt matrix `matrix` (host, row-major,
+ * state dtype) to `targets` (nt qubits, listed order = matrix bit order R3),
+ * controlled on `controls` (nc qubits, may be NULL when nc == 0).  `n` must
+ * equal the state's qubit count (S:124 ShapeMismatch -> INVALID_ARG). */
+qj_status qj_apply_gate(qj_state s, int n, const int* targets, int nt,
+                        const int* controls, int nc, const void* matrix);
+
+/* Specialised operators: amplitude permutations / sign
+ * flips with no arithmetic; results are exact (IEEE ==) vs Eq. 1. */
+qj_status qj_apply_x(qj_state s, int target, const int* controls, int nc);
+qj_status qj_apply_z(qj_state s, int target, const int* controls, int nc);
+qj_status qj_apply_swap(qj_state s, int t0, int t1, const int* controls, int nc);
+
+/* fSim: [[1,0,0,0],[0,u00,u01,0],[0,u10,u11,0],[0,0,0,phase11]] on (t0, t1)
+ * (t0 = MSB).  u2x2: 4 complex (row-major), phase11: 1 complex (e^{-i phi}). */
+qj_status qj_apply_fsim(qj_state s, int t0, int t1, const void* u2x2, const void* phase11,
+                        const int* controls, int nc);
+
+/* Diagonal gate: psi_i <- diag[row(i)] psi_i, row(i) = target bits of i in
+ * listed order (first = MSB); `diag` = 2^nt complex values. */
+qj_status qj_apply_diagonal(qj_state s, const int* targets, int nt, const void* diag,
+                            const int* controls, int nc);
+
+/* ---- circuits --------------------------------------------------------------- */
+typedef enum {
+    QJ_GATE_DENSE = 0,   /* data: 4^nt complex (row-major matrix)       */
+    QJ_GATE_X = 1,       /* data: unused                                */
+    QJ_GATE_Z = 2,       /* data: unused                                */
+    QJ_GATE_SWAP = 3,    /* data: unused (nt == 2)                      */
+    QJ_GATE_FSIM = 4,    /* data: 5 complex: u00,u01,u10,u11,phase11    */
+    QJ_GATE_DIAG = 5     /* data: 2^nt complex                          */
+} qj_gate_kind;
+
+typedef struct {
+    int kind;
+    int nt;
+    int nc;
+    int targets[QJ_MAX_TARGETS];
+    int controls[QJ_MAX_CONTROLS];
+    const void* data;    /* host pointer, state dtype, read before return */
+} qj_gate;
+
+#define QJ_FUSE 1u       /* plan runs of gates into fused window tile passes */
+
+/* Apply `ngates` gates in order.  Without QJ_FUSE every gate is one pass as
+ * if issued through the single-gate entry points.  With QJ_FUSE the planner
+ * groups runs of consecutive gates into window passes (one HBM round trip per
+ * run, PAPER.md:539-550 fusion, done B200-style); results agree with the
+ * unfused path within floating-point tolerance.  All gates are validated
+ * before anything is enqueued. */
+qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_t flags);
+
+/* ---- readout -----------------------------------------------------------------
+ * Born-rule probabilities.  qubits == NULL and nq == -1:
+ * the full vector |psi_i|^2 in canonical index order (2^n values).  Otherwise
+ * the marginal over the listed qubits, first listed = most significant bit of
+ * the output index (2^nq values, accumulated in fp64).  `out_dev` is caller
+ * owned DEVICE memory of the state's real type (float for C64, double for
+ * C128).  Sharded states: out_dev must hold the full output. */
+qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev);
+
+/* Block until all work enqueued on the handle has finished; reports
+ * asynchronous CUDA errors. */
+qj_status qj_sync(qj_state s);
+
+/* ---- introspection -------------------------------------------------------- */
+typedef struct {
+    uint64_t launches;       /* kernels launched by the library                  */
+    uint64_t passes;         /* state passes (gate or fused window passes)       */
+    uint64_t exchanges;      /* global<->local qubit swaps (sharded states)      */
+    double alg_bytes;        /* algorithmic HBM bytes of all passes (C15)        */
+    double exchange_bytes;   /* bytes moved by exchanges                          */
+} qj_counters;
+
+qj_status qj_get_counters(qj_state s, qj_counters* out, int reset);
+
+/* n, local qubits, dtype, number of shards of the handle. */
+qj_status qj_state_info(qj_state s, int* n, int* n_local, int* dtype, int* nshards);
+
+/* Thread-local message describing the last failure ("" if none). */
+const char* qj_last_error(void);
+
+/* Library version string. */
+const char* qj_version(void);
+
+/* Host-side index math used by every pass (exported for exhaustive CPU
+ * tests): insert a 0 bit at each of the `npos` ascending bit positions
+ * `sorted_pos` into g (PAPER.md:221-227 listing, i1 = ((g>>m)<<(m+1)) + (g & (k-1))). */
+uint64_t qj_insert_zero_bits(uint64_t g, const int* sorted_pos, int npos);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QJ_H */

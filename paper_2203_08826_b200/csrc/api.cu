@@ -1,0 +1,470 @@
+// api.cu -- the C ABI of libqj (include/qj.h): validation, the per-gate
+// planner (logical qubits -> physical bit positions, specialisation, sharded
+// global-qubit handling) and dispatch to the sm_100a pass kernels.
+//
+// Nothing here does amplitude arithmetic: every amplitude is touched by a
+// kernel in kernels.cuh / tile_pass.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qj_internal.h"
+#include "planner.h"
+#include "common.cuh"
+
+using namespace qj;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static qj_status fail(qj_status code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+static qj_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(QJ_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ handle
+struct qj_state_s {
+    int n = 0, nl = 0, g = 0;
+    qj_dtype dt = QJ_C128;
+    int amp_bytes = 16;
+    std::vector<void*> shards;
+    cudaStream_t stream = nullptr;
+    std::vector<int> phys;  // logical qubit -> physical bit (bits >= nl are global)
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    double* bins = nullptr;
+    size_t bins_cap = 0;  // doubles
+    LaunchStats ls;
+    qj_counters ctr{};
+    Planner planner;
+};
+
+namespace {
+
+bool dtype_ok(int dt) { return dt == QJ_C64 || dt == QJ_C128; }
+
+template <typename F>
+cudaError_t by_dtype(qj_dtype dt, F&& f) {
+    if (dt == QJ_C64) return f((float)0);
+    return f((double)0);
+}
+
+qj_status ensure_scratch(qj_state s, size_t bytes) {
+    if (s->scratch_bytes >= bytes) return QJ_OK;
+    if (s->scratch) {
+        cudaStreamSynchronize(s->stream);
+        cudaFree(s->scratch);
+        s->scratch = nullptr;
+        s->scratch_bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&s->scratch, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch alloc");
+    s->scratch_bytes = bytes;
+    return QJ_OK;
+}
+
+qj_status ensure_bins(qj_state s, size_t nb) {
+    if (s->bins_cap >= nb) return QJ_OK;
+    if (s->bins) {
+        cudaStreamSynchronize(s->stream);
+        cudaFree(s->bins);
+        s->bins = nullptr;
+        s->bins_cap = 0;
+    }
+    cudaError_t e = cudaMalloc(&s->bins, nb * sizeof(double));
+    if (e != cudaSuccess) return cuda_fail(e, "bins alloc");
+    s->bins_cap = nb;
+    return QJ_OK;
+}
+
+// Read a host complex array of the state's dtype into complex<double>.
+std::vector<cd> read_complex(const void* p, size_t count, qj_dtype dt) {
+    std::vector<cd> v(count);
+    if (dt == QJ_C64) {
+        const float* f = static_cast<const float*>(p);
+        for (size_t i = 0; i < count; ++i) v[i] = cd(f[2 * i], f[2 * i + 1]);
+    } else {
+        const double* d = static_cast<const double*>(p);
+        for (size_t i = 0; i < count; ++i) v[i] = cd(d[2 * i], d[2 * i + 1]);
+    }
+    return v;
+}
+
+qj_status validate_qubits(qj_state s, const int* targets, int nt, const int* controls, int nc) {
+    if (nt < 1) return fail(QJ_ERR_INVALID_ARG, "nt must be >= 1 (got %d)", nt);
+    if (nt > QJ_MAX_TARGETS) return fail(QJ_ERR_TOO_MANY_TARGETS, "nt=%d exceeds %d", nt, QJ_MAX_TARGETS);
+    if (nc < 0) return fail(QJ_ERR_INVALID_ARG, "nc must be >= 0 (got %d)", nc);
+    if (nc > QJ_MAX_CONTROLS) return fail(QJ_ERR_TOO_MANY_TARGETS, "nc=%d exceeds %d", nc, QJ_MAX_CONTROLS);
+    if (!targets) return fail(QJ_ERR_INVALID_ARG, "targets is NULL");
+    if (nc > 0 && !controls) return fail(QJ_ERR_INVALID_ARG, "controls is NULL with nc=%d", nc);
+    uint64_t seen_lo = 0, seen_hi = 0;
+    auto check = [&](int q, const char* what) -> qj_status {
+        if (q < 0 || q >= s->n) return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "%s qubit %d out of range [0,%d)", what, q, s->n);
+        uint64_t& w = q < 64 ? seen_lo : seen_hi;
+        const uint64_t b = 1ull << (q & 63);
+        if (w & b) return fail(QJ_ERR_OVERLAPPING_QUBITS, "qubit %d listed twice (targets and controls must be disjoint)", q);
+        w |= b;
+        return QJ_OK;
+    };
+    for (int i = 0; i < nt; ++i)
+        if (qj_status st = check(targets[i], "target")) return st;
+    for (int i = 0; i < nc; ++i)
+        if (qj_status st = check(controls[i], "control")) return st;
+    return QJ_OK;
+}
+
+// Convert an ABI gate into a logical gate (validated).
+qj_status make_lgate(qj_state s, int kind, const int* targets, int nt, const int* controls, int nc,
+                     const void* data, LGate& out) {
+    if (qj_status st = validate_qubits(s, targets, nt, controls, nc)) return st;
+    out = LGate();
+    out.kind = kind;
+    out.nt = nt;
+    out.nc = nc;
+    for (int i = 0; i < nt; ++i) out.t[i] = targets[i];
+    for (int i = 0; i < nc; ++i) out.c[i] = controls[i];
+    switch (kind) {
+        case QJ_GATE_DENSE:
+            if (!data) return fail(QJ_ERR_INVALID_ARG, "matrix is NULL");
+            out.data = read_complex(data, (size_t)1 << (2 * nt), s->dt);
+            break;
+        case QJ_GATE_X:
+        case QJ_GATE_Z:
+            if (nt != 1) return fail(QJ_ERR_INVALID_ARG, "X/Z take exactly one target (got %d)", nt);
+            break;
+        case QJ_GATE_SWAP:
+            if (nt != 2) return fail(QJ_ERR_INVALID_ARG, "SWAP takes exactly two targets (got %d)", nt);
+            break;
+        case QJ_GATE_FSIM:
+            if (nt != 2) return fail(QJ_ERR_INVALID_ARG, "fSim takes exactly two targets (got %d)", nt);
+            if (!data) return fail(QJ_ERR_INVALID_ARG, "fSim parameters are NULL");
+            out.data = read_complex(data, 5, s->dt);
+            break;
+        case QJ_GATE_DIAG:
+            if (!data) return fail(QJ_ERR_INVALID_ARG, "diagonal is NULL");
+            out.data = read_complex(data, (size_t)1 << nt, s->dt);
+            break;
+        default:
+            return fail(QJ_ERR_INVALID_ARG, "unknown gate kind %d", kind);
+    }
+    return QJ_OK;
+}
+
+// Execute planned steps on the device.
+qj_status execute(qj_state s, const std::vector<Step>& steps) {
+    cudaError_t e = cudaSuccess;
+    for (const Step& st : steps) {
+        if (st.type == Step::EXCHANGE) {
+            // swap global bit (nl + j) with local bit L: pair shards r (bit j = 0) and r | 1<<j
+            const int j = st.gbit, L = st.lbit;
+            for (size_t r = 0; r < s->shards.size(); ++r) {
+                if ((r >> j) & 1) continue;
+                const size_t r2 = r | (1ull << j);
+                e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return run_exchange<R>(s->shards[r], s->shards[r2], s->nl, L, s->stream, s->ls);
+                });
+                if (e != cudaSuccess) return cuda_fail(e, "exchange launch");
+            }
+            s->ctr.exchanges++;
+            s->ctr.exchange_bytes += (double)s->amp_bytes * (double)(1ull << s->nl) * (double)s->shards.size();
+            continue;
+        }
+        if (st.pass.k > 5 && st.pass.kind == PK_DENSE) {
+            const size_t need = (size_t)s->amp_bytes * ((size_t)1 << (2 * st.pass.k));
+            if (qj_status q = ensure_scratch(s, need)) return q;
+        }
+        e = by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            if (st.type == Step::TILE) return run_tile<R>(st.tile, s->shards[st.shard], s->nl, s->stream, s->ls);
+            return run_pass<R>(st.pass, s->shards[st.shard], s->nl, s->stream, s->scratch, s->scratch_bytes, s->ls);
+        });
+        if (e != cudaSuccess) return cuda_fail(e, "pass launch");
+        s->ctr.passes++;
+        s->ctr.alg_bytes += st.alg_bytes;
+    }
+    s->ctr.launches = s->ls.launches;
+    return QJ_OK;
+}
+
+qj_status apply_lgates(qj_state s, const std::vector<LGate>& gates, bool fuse) {
+    std::vector<Step> steps;
+    PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, (int)s->shards.size(), &s->phys};
+    s->planner.plan(ctx, gates, fuse, steps);
+    return execute(s, steps);
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+const char* qj_last_error(void) { return g_err.c_str(); }
+
+const char* qj_version(void) { return "qj 0.1 (sm_100a)"; }
+
+uint64_t qj_insert_zero_bits(uint64_t g, const int* sorted_pos, int npos) {
+    for (int i = 0; i < npos; ++i) g = insert_zero(g, sorted_pos[i]);
+    return g;
+}
+
+static qj_status init_common(qj_state* out, void* const* shards, int nshards, int n, qj_dtype dt,
+                             uint64_t basis_index, void* cuda_stream) {
+    if (!out) return fail(QJ_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!dtype_ok(dt)) return fail(QJ_ERR_DTYPE, "unknown dtype %d", (int)dt);
+    if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
+    if (nshards < 1 || (nshards & (nshards - 1))) return fail(QJ_ERR_INVALID_ARG, "nshards=%d is not a power of two", nshards);
+    int g = 0;
+    while ((1 << g) < nshards) ++g;
+    if (g >= n) return fail(QJ_ERR_CAPACITY, "%d shards need more than n=%d qubits", nshards, n);
+    if (!shards) return fail(QJ_ERR_INVALID_ARG, "amplitude buffer is NULL");
+    for (int r = 0; r < nshards; ++r) {
+        if (!shards[r]) return fail(QJ_ERR_INVALID_ARG, "shard %d buffer is NULL", r);
+        if (reinterpret_cast<uintptr_t>(shards[r]) & 15u)
+            return fail(QJ_ERR_INVALID_ARG, "shard %d buffer is not 16-byte aligned", r);
+    }
+    if (basis_index != QJ_KEEP && n < 64 && basis_index >= (1ull << n))
+        return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "basis_index %llu >= 2^%d", (unsigned long long)basis_index, n);
+    qj_state s = new (std::nothrow) qj_state_s;
+    if (!s) return fail(QJ_ERR_CAPACITY, "out of host memory");
+    s->n = n;
+    s->g = g;
+    s->nl = n - g;
+    s->dt = dt;
+    s->amp_bytes = dt == QJ_C64 ? 8 : 16;
+    s->shards.assign(shards, shards + nshards);
+    s->stream = static_cast<cudaStream_t>(cuda_stream);
+    s->phys.resize(n);
+    for (int q = 0; q < n; ++q) s->phys[q] = n - 1 - q;  // reading R1
+    *out = s;
+    if (basis_index != QJ_KEEP) {
+        qj_status st = qj_state_reset(s, basis_index);
+        if (st != QJ_OK) {
+            delete s;
+            *out = nullptr;
+            return st;
+        }
+    }
+    return QJ_OK;
+}
+
+qj_status qj_state_init(qj_state* out, void* amps_dev, int n, qj_dtype dt, uint64_t basis_index, void* cuda_stream,
+                        void* nccl_comm) {
+    if (nccl_comm != nullptr)
+        return fail(QJ_ERR_UNSUPPORTED, "NCCL-sharded states are created with qj_state_init_nccl");
+    void* shards[1] = {amps_dev};
+    return init_common(out, shards, 1, n, dt, basis_index, cuda_stream);
+}
+
+qj_status qj_state_init_sharded(qj_state* out, void* const* shards, int nshards, int n, qj_dtype dt,
+                                uint64_t basis_index, void* cuda_stream) {
+    return init_common(out, shards, nshards, n, dt, basis_index, cuda_stream);
+}
+
+qj_status qj_state_reset(qj_state s, uint64_t basis_index) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (basis_index == QJ_KEEP) return QJ_OK;
+    if (s->n < 64 && basis_index >= (1ull << s->n))
+        return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "basis_index %llu >= 2^%d", (unsigned long long)basis_index, s->n);
+    for (int q = 0; q < s->n; ++q) s->phys[q] = s->n - 1 - q;
+    const uint64_t owner = basis_index >> s->nl;
+    const uint64_t local = basis_index & ((1ull << s->nl) - 1);
+    for (size_t r = 0; r < s->shards.size(); ++r) {
+        cudaError_t e = by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            return run_init<R>(s->shards[r], s->nl, local, r == owner, s->stream, s->ls);
+        });
+        if (e != cudaSuccess) return cuda_fail(e, "init launch");
+    }
+    s->ctr.launches = s->ls.launches;
+    return QJ_OK;
+}
+
+qj_status qj_state_free(qj_state s) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (s->scratch || s->bins) cudaStreamSynchronize(s->stream);
+    if (s->scratch) cudaFree(s->scratch);
+    if (s->bins) cudaFree(s->bins);
+    delete s;
+    return QJ_OK;
+}
+
+qj_status qj_state_info(qj_state s, int* n, int* n_local, int* dtype, int* nshards) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (n) *n = s->n;
+    if (n_local) *n_local = s->nl;
+    if (dtype) *dtype = (int)s->dt;
+    if (nshards) *nshards = (int)s->shards.size();
+    return QJ_OK;
+}
+
+qj_status qj_get_counters(qj_state s, qj_counters* out, int reset) {
+    if (!s || !out) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
+    s->ctr.launches = s->ls.launches;
+    *out = s->ctr;
+    if (reset) {
+        s->ctr = qj_counters{};
+        s->ls.launches = 0;
+    }
+    return QJ_OK;
+}
+
+static qj_status apply_one(qj_state s, int kind, const int* targets, int nt, const int* controls, int nc,
+                           const void* data) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    std::vector<LGate> gs(1);
+    if (qj_status st = make_lgate(s, kind, targets, nt, controls, nc, data, gs[0])) return st;
+    return apply_lgates(s, gs, false);
+}
+
+qj_status qj_apply_gate(qj_state s, int n, const int* targets, int nt, const int* controls, int nc,
+                        const void* matrix) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (n != s->n) return fail(QJ_ERR_INVALID_ARG, "n=%d does not match the state's n=%d", n, s->n);
+    return apply_one(s, QJ_GATE_DENSE, targets, nt, controls, nc, matrix);
+}
+
+qj_status qj_apply_x(qj_state s, int target, const int* controls, int nc) {
+    return apply_one(s, QJ_GATE_X, &target, 1, controls, nc, nullptr);
+}
+
+qj_status qj_apply_z(qj_state s, int target, const int* controls, int nc) {
+    return apply_one(s, QJ_GATE_Z, &target, 1, controls, nc, nullptr);
+}
+
+qj_status qj_apply_swap(qj_state s, int t0, int t1, const int* controls, int nc) {
+    const int t[2] = {t0, t1};
+    return apply_one(s, QJ_GATE_SWAP, t, 2, controls, nc, nullptr);
+}
+
+qj_status qj_apply_fsim(qj_state s, int t0, int t1, const void* u2x2, const void* phase11, const int* controls,
+                        int nc) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (!u2x2 || !phase11) return fail(QJ_ERR_INVALID_ARG, "fSim parameters are NULL");
+    // pack (u00,u01,u10,u11,phase11) contiguously in the state's dtype
+    const size_t cb = (size_t)s->amp_bytes;
+    unsigned char buf[5 * 16];
+    std::memcpy(buf, u2x2, 4 * cb);
+    std::memcpy(buf + 4 * cb, phase11, cb);
+    const int t[2] = {t0, t1};
+    return apply_one(s, QJ_GATE_FSIM, t, 2, controls, nc, buf);
+}
+
+qj_status qj_apply_diagonal(qj_state s, const int* targets, int nt, const void* diag, const int* controls, int nc) {
+    return apply_one(s, QJ_GATE_DIAG, targets, nt, controls, nc, diag);
+}
+
+qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_t flags) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (ngates < 0) return fail(QJ_ERR_INVALID_ARG, "ngates=%d < 0", ngates);
+    if (ngates > 0 && !gates) return fail(QJ_ERR_INVALID_ARG, "gates is NULL");
+    if (flags & ~QJ_FUSE) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    std::vector<LGate> gs((size_t)ngates);
+    for (int i = 0; i < ngates; ++i) {
+        const qj_gate& g = gates[i];
+        if (g.nt > QJ_MAX_TARGETS || g.nc > QJ_MAX_CONTROLS)
+            return fail(QJ_ERR_TOO_MANY_TARGETS, "gate %d: nt=%d nc=%d exceeds the limits", i, g.nt, g.nc);
+        qj_status st = make_lgate(s, g.kind, g.targets, g.nt, g.controls, g.nc, g.data, gs[(size_t)i]);
+        if (st != QJ_OK) {
+            g_err = "gate " + std::to_string(i) + ": " + g_err;
+            return st;
+        }
+    }
+    return apply_lgates(s, gs, (flags & QJ_FUSE) != 0);
+}
+
+qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (!out_dev) return fail(QJ_ERR_INVALID_ARG, "out_dev is NULL");
+    cudaError_t e = cudaSuccess;
+    const int n = s->n, nl = s->nl;
+    if (qubits == nullptr && nq == -1) {
+        bool identity = true;
+        for (int q = 0; q < n; ++q) identity &= (s->phys[q] == n - 1 - q);
+        const size_t rb = s->dt == QJ_C64 ? 4 : 8;
+        for (size_t r = 0; r < s->shards.size(); ++r) {
+            if (identity) {
+                void* dst = static_cast<unsigned char*>(out_dev) + rb * (r << nl);
+                e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return run_prob_full<R>(s->shards[r], nl, dst, s->stream, s->ls);
+                });
+            } else {
+                int cpos[64];
+                for (int q = 0; q < n; ++q) cpos[s->phys[q]] = n - 1 - q;
+                e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return run_prob_scatter<R>(s->shards[r], nl, r, n, cpos, out_dev, s->stream, s->ls);
+                });
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "probabilities launch");
+        }
+        s->ctr.launches = s->ls.launches;
+        return QJ_OK;
+    }
+    if (!qubits) return fail(QJ_ERR_INVALID_ARG, "qubits is NULL (use nq=-1 for the full vector)");
+    if (nq < 1 || nq > n) return fail(QJ_ERR_INVALID_ARG, "nq=%d outside [1,%d]", nq, n);
+    if (nq > 30) return fail(QJ_ERR_CAPACITY, "marginal over %d qubits is too large (max 30)", nq);
+    uint64_t seen_lo = 0;
+    for (int i = 0; i < nq; ++i) {
+        const int q = qubits[i];
+        if (q < 0 || q >= n) return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "qubit %d out of range [0,%d)", q, n);
+        if (seen_lo & (1ull << q)) return fail(QJ_ERR_OVERLAPPING_QUBITS, "qubit %d listed twice", q);
+        seen_lo |= 1ull << q;
+    }
+    const size_t nb = (size_t)1 << nq;
+    if (qj_status st = ensure_bins(s, nb)) return st;
+    e = cudaMemsetAsync(s->bins, 0, nb * sizeof(double), s->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "bins memset");
+    for (size_t r = 0; r < s->shards.size(); ++r) {
+        int pos[64], gv[64];
+        for (int i = 0; i < nq; ++i) {
+            const int b = s->phys[qubits[i]];
+            if (b < nl) {
+                pos[i] = b;
+                gv[i] = 0;
+            } else {
+                pos[i] = -1;
+                gv[i] = (int)((r >> (b - nl)) & 1u);
+            }
+        }
+        e = by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            return run_prob_marginal<R>(s->shards[r], nl, pos, gv, nq, s->bins, s->stream, s->ls);
+        });
+        if (e != cudaSuccess) return cuda_fail(e, "marginal launch");
+    }
+    e = by_dtype(s->dt, [&](auto z) {
+        using R = decltype(z);
+        return run_bins_to_out<R>(s->bins, nb, out_dev, s->stream, s->ls);
+    });
+    if (e != cudaSuccess) return cuda_fail(e, "bins launch");
+    s->ctr.launches = s->ls.launches;
+    return QJ_OK;
+}
+
+qj_status qj_sync(qj_state s) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    cudaError_t e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "qj_sync");
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "qj_sync");
+    return QJ_OK;
+}
+
+}  // extern "C"

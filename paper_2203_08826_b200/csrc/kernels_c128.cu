@@ -1,0 +1,5 @@
+// complex128 instantiation of the single-gate pass kernels (see kernels.cuh).
+#include "kernels.cuh"
+namespace qj {
+QJ_INSTANTIATE(double)
+}

@@ -1,0 +1,72 @@
+// qj_internal.h -- host-side types shared by the C-ABI layer, the planner and
+// the kernel launchers of libqj (never exposed through include/qj.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <complex>
+#include <string>
+#include <vector>
+
+#include "../../include/qj.h"
+
+namespace qj {
+
+using cd = std::complex<double>;
+
+// One planned pass over ONE shard.  Bit positions are PHYSICAL positions of
+// the shard's local index (0 = least significant).
+enum PassKind {
+    PK_DENSE = 0,  // 2^k x 2^k matrix on k targets (Eq. 1), member `touch` mask
+    PK_X = 1,      // X on 1 target: swap pairs (no arithmetic)
+    PK_SWAP = 2,   // SWAP on 2 targets: exchange the |01>,|10> members
+    PK_DIAG = 3,   // psi_i <- diag[row(i)] psi_i over k targets
+    PK_PHASE = 4,  // psi_i <- phase * psi_i on the subspace fixed by `fix`
+    PK_NEG = 5,    // psi_i <- -psi_i on the subspace fixed by `fix` (Z, CZ, ...)
+};
+
+struct Pass {
+    int kind = PK_DENSE;
+    int k = 0;                 // number of targets (DENSE/X/SWAP/DIAG)
+    int tpos[QJ_MAX_TARGETS];  // target bit positions, listed (= matrix) order
+    int nfix = 0;              // positions whose bit value is fixed (controls, phase pattern)
+    int fpos[64];
+    int fval[64];
+    uint32_t touch = 0xffffffffu;  // DENSE: member mask over the listed-order member index
+    std::vector<cd> m;             // DENSE: 4^k row-major; DIAG: 2^k; PHASE: 1
+};
+
+struct LaunchStats {
+    uint64_t launches = 0;
+};
+
+// Algorithmic HBM bytes of a pass on a shard of 2^nl amplitudes of `bytes_per_amp`
+// (C15: 2 * s * number of amplitudes the pass must change).
+double pass_alg_bytes(const Pass& p, int nl, int bytes_per_amp);
+
+// Launchers (kernels_*.cu).  R = float (complex64) or double (complex128).
+template <typename R>
+cudaError_t run_pass(const Pass& p, void* psi, int nl, cudaStream_t st, void* scratch,
+                     size_t scratch_bytes, LaunchStats& ls);
+template <typename R>
+cudaError_t run_init(void* psi, int nl, uint64_t basis_local, bool set_one, cudaStream_t st,
+                     LaunchStats& ls);
+// probabilities of one shard: full (nq < 0, out = R[2^nl]) or marginal
+// accumulated (fp64 atomics) into bins[2^nq]; positions = physical bits
+// (pos < 0 means a global bit with value given by gbits).
+template <typename R>
+cudaError_t run_prob_full(const void* psi, int nl, void* out, cudaStream_t st, LaunchStats& ls);
+template <typename R>
+cudaError_t run_prob_marginal(const void* psi, int nl, const int* pos, const int* gval, int nq,
+                              double* bins, cudaStream_t st, LaunchStats& ls);
+template <typename R>
+cudaError_t run_bins_to_out(const double* bins, uint64_t nbins, void* out, cudaStream_t st,
+                            LaunchStats& ls);
+template <typename R>
+cudaError_t run_prob_scatter(const void* psi, int nl, uint64_t shard, int n, const int* cpos, void* out,
+                             cudaStream_t st, LaunchStats& ls);
+template <typename R>
+cudaError_t run_exchange(void* a, void* b, int nl, int L, cudaStream_t st, LaunchStats& ls);
+
+}  // namespace qj

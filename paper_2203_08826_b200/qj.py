@@ -1,0 +1,271 @@
+"""Thin ctypes binding of libqj (include/qj.h).  Argument marshalling only:
+every amplitude is touched by the library's sm_100a kernels.  torch supplies
+device memory and streams; nothing here computes on the state.
+
+The library is built in-tree (``python -m paper_2203_08826_b200.build``); if it
+is missing, importing this module raises -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libqj.so")
+
+QJ_C64, QJ_C128 = 0, 1
+QJ_KEEP = (1 << 64) - 1
+QJ_FUSE = 1
+MAX_TARGETS, MAX_CONTROLS = 8, 16
+KIND = {"dense": 0, "x": 1, "z": 2, "swap": 3, "fsim": 4, "diag": 5}
+STATUS = {0: "QJ_OK", 1: "QJ_ERR_INVALID_ARG", 2: "QJ_ERR_INDEX_OUT_OF_RANGE",
+          3: "QJ_ERR_OVERLAPPING_QUBITS", 4: "QJ_ERR_TOO_MANY_TARGETS", 5: "QJ_ERR_CAPACITY",
+          6: "QJ_ERR_DTYPE", 7: "QJ_ERR_CUDA", 8: "QJ_ERR_NCCL", 9: "QJ_ERR_UNSUPPORTED"}
+
+EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state_free",
+           "qj_apply_gate", "qj_apply_x", "qj_apply_z", "qj_apply_swap", "qj_apply_fsim",
+           "qj_apply_diagonal", "qj_apply_circuit", "qj_probabilities", "qj_sync",
+           "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
+           "qj_insert_zero_bits"]
+
+
+class QJError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class qj_gate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("nt", ctypes.c_int), ("nc", ctypes.c_int),
+                ("targets", ctypes.c_int * MAX_TARGETS), ("controls", ctypes.c_int * MAX_CONTROLS),
+                ("data", ctypes.c_void_p)]
+
+
+class qj_counters(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_uint64), ("passes", ctypes.c_uint64),
+                ("exchanges", ctypes.c_uint64), ("alg_bytes", ctypes.c_double),
+                ("exchange_bytes", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libqj.so (raises if the CUDA library has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libqj.so not built: run `python -m paper_2203_08826_b200.build` ({LIB_PATH})")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, U64, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_int
+    IP = ctypes.POINTER(ctypes.c_int)
+    sig = {
+        "qj_state_init": ([ctypes.POINTER(P), P, I, I, U64, P, P], S),
+        "qj_state_init_sharded": ([ctypes.POINTER(P), ctypes.POINTER(P), I, I, I, U64, P], S),
+        "qj_state_reset": ([P, U64], S),
+        "qj_state_free": ([P], S),
+        "qj_apply_gate": ([P, I, IP, I, IP, I, P], S),
+        "qj_apply_x": ([P, I, IP, I], S),
+        "qj_apply_z": ([P, I, IP, I], S),
+        "qj_apply_swap": ([P, I, I, IP, I], S),
+        "qj_apply_fsim": ([P, I, I, P, P, IP, I], S),
+        "qj_apply_diagonal": ([P, IP, I, P, IP, I], S),
+        "qj_apply_circuit": ([P, ctypes.POINTER(qj_gate), I, ctypes.c_uint32], S),
+        "qj_probabilities": ([P, IP, I, P], S),
+        "qj_sync": ([P], S),
+        "qj_get_counters": ([P, ctypes.POINTER(qj_counters), I], S),
+        "qj_state_info": ([P, IP, IP, IP, IP], S),
+        "qj_last_error": ([], ctypes.c_char_p),
+        "qj_version": ([], ctypes.c_char_p),
+        "qj_insert_zero_bits": ([U64, IP, I], U64),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code != 0:
+        raise QJError(code, lib().qj_last_error().decode())
+
+
+def _ints(xs):
+    xs = [int(x) for x in (xs or ())]
+    return (ctypes.c_int * max(1, len(xs)))(*xs), len(xs)
+
+
+def insert_zero_bits(g: int, sorted_positions) -> int:
+    arr, n = _ints(sorted_positions)
+    return int(lib().qj_insert_zero_bits(ctypes.c_uint64(g), arr, n))
+
+
+class State:
+    """A state vector living in caller-owned torch device memory.
+
+    ``State(tensor, basis=0)`` wraps a contiguous complex64/complex128 CUDA
+    tensor of 2^n elements and writes |basis> into it (``basis=None`` keeps the
+    contents).  ``State.sharded([t0, t1, ...], n)`` wraps 2^g shards of
+    2^(n-g) amplitudes (global qubits = the top g bits)."""
+
+    def __init__(self, tensor=None, basis=0, stream=None, _shards=None, _n=None):
+        import torch
+
+        L = lib()
+        self._h = ctypes.c_void_p()
+        shards = _shards if _shards is not None else [tensor]
+        t0 = shards[0]
+        for t in shards:
+            if not (t.is_cuda and t.is_contiguous()):
+                raise ValueError("state tensors must be contiguous CUDA tensors")
+            if t.dtype not in (torch.complex64, torch.complex128) or t.dtype != t0.dtype:
+                raise ValueError("state tensors must all be complex64 or all complex128")
+        self.dtype = QJ_C64 if t0.dtype == torch.complex64 else QJ_C128
+        self.np_dtype = np.complex64 if self.dtype == QJ_C64 else np.complex128
+        self.real_dtype = torch.float32 if self.dtype == QJ_C64 else torch.float64
+        ntot = _n if _n is not None else int(t0.numel()).bit_length() - 1
+        if _n is None and (1 << ntot) != t0.numel():
+            raise ValueError("state length must be a power of two")
+        self.n = ntot
+        self.shards = shards
+        self.device = t0.device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        basis = QJ_KEEP if basis is None else int(basis)
+        if _shards is None:
+            _check(L.qj_state_init(ctypes.byref(self._h), ctypes.c_void_p(t0.data_ptr()), ntot, self.dtype,
+                                   ctypes.c_uint64(basis), ctypes.c_void_p(self.stream.cuda_stream), None))
+        else:
+            ptrs = (ctypes.c_void_p * len(shards))(*[t.data_ptr() for t in shards])
+            _check(L.qj_state_init_sharded(ctypes.byref(self._h), ptrs, len(shards), ntot, self.dtype,
+                                           ctypes.c_uint64(basis), ctypes.c_void_p(self.stream.cuda_stream)))
+
+    @classmethod
+    def sharded(cls, shards, n, basis=0, stream=None):
+        return cls(None, basis=basis, stream=stream, _shards=list(shards), _n=n)
+
+    # -- lifetime ----------------------------------------------------------
+    def free(self):
+        if self._h:
+            _check(lib().qj_state_free(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def reset(self, basis=0):
+        _check(lib().qj_state_reset(self._h, ctypes.c_uint64(QJ_KEEP if basis is None else basis)))
+
+    def sync(self):
+        _check(lib().qj_sync(self._h))
+
+    # -- gates -------------------------------------------------------------
+    def _mat(self, m, count):
+        a = np.ascontiguousarray(np.asarray(m, dtype=self.np_dtype).reshape(-1))
+        if a.size != count:
+            raise ValueError(f"expected {count} complex values, got {a.size}")
+        return a
+
+    def apply_gate(self, targets, matrix, controls=()):
+        t, nt = _ints(targets)
+        c, nc = _ints(controls)
+        m = self._mat(matrix, 4 ** nt)
+        _check(lib().qj_apply_gate(self._h, self.n, t, nt, c, nc, ctypes.c_void_p(m.ctypes.data)))
+
+    def x(self, target, controls=()):
+        c, nc = _ints(controls)
+        _check(lib().qj_apply_x(self._h, int(target), c, nc))
+
+    def z(self, target, controls=()):
+        c, nc = _ints(controls)
+        _check(lib().qj_apply_z(self._h, int(target), c, nc))
+
+    def swap(self, t0, t1, controls=()):
+        c, nc = _ints(controls)
+        _check(lib().qj_apply_swap(self._h, int(t0), int(t1), c, nc))
+
+    def fsim(self, t0, t1, u2x2, phase11, controls=()):
+        c, nc = _ints(controls)
+        u = self._mat(u2x2, 4)
+        p = self._mat([phase11], 1)
+        _check(lib().qj_apply_fsim(self._h, int(t0), int(t1), ctypes.c_void_p(u.ctypes.data),
+                                   ctypes.c_void_p(p.ctypes.data), c, nc))
+
+    def diagonal(self, targets, diag, controls=()):
+        t, nt = _ints(targets)
+        c, nc = _ints(controls)
+        d = self._mat(diag, 2 ** nt)
+        _check(lib().qj_apply_diagonal(self._h, t, nt, ctypes.c_void_p(d.ctypes.data), c, nc))
+
+    def pack_circuit(self, gates):
+        """Marshal gate records (objects with kind/targets/controls/data, e.g.
+        workloads.gates.Gate) into a qj_gate array; returns (array, keepalive)."""
+        gates = list(gates)
+        arr = (qj_gate * max(1, len(gates)))()
+        keep = []
+        for i, g in enumerate(gates):
+            e = arr[i]
+            e.kind = KIND[g.kind]
+            e.nt = len(g.targets)
+            e.nc = len(g.controls)
+            if e.nt > MAX_TARGETS or e.nc > MAX_CONTROLS:
+                raise QJError(4, f"gate {i}: too many qubits")
+            for j, q in enumerate(g.targets):
+                e.targets[j] = int(q)
+            for j, q in enumerate(g.controls):
+                e.controls[j] = int(q)
+            if g.kind == "dense":
+                d = self._mat(g.data[0], 4 ** e.nt)
+            elif g.kind == "diag":
+                d = self._mat(g.data[0], 2 ** e.nt)
+            elif g.kind == "fsim":
+                d = self._mat(list(np.asarray(g.data[0]).reshape(-1)) + [g.data[1]], 5)
+            else:
+                d = None
+            if d is not None:
+                keep.append(d)
+                e.data = d.ctypes.data
+            else:
+                e.data = None
+        return arr, len(gates), keep
+
+    def apply_circuit(self, gates, fuse=False, packed=None):
+        arr, ng, keep = packed if packed is not None else self.pack_circuit(gates)
+        _check(lib().qj_apply_circuit(self._h, arr, ng, QJ_FUSE if fuse else 0))
+        del keep
+
+    # -- readout -----------------------------------------------------------
+    def probabilities(self, qubits=None, out=None):
+        import torch
+
+        if qubits is None:
+            size = 1 << self.n
+            q, nq = None, -1
+        else:
+            qa, nq = _ints(qubits)
+            q = qa
+            size = 1 << nq
+        if out is None:
+            out = torch.empty(size, dtype=self.real_dtype, device=self.device)
+        _check(lib().qj_probabilities(self._h, q, nq, ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def counters(self, reset=False):
+        c = qj_counters()
+        _check(lib().qj_get_counters(self._h, ctypes.byref(c), 1 if reset else 0))
+        return {"launches": c.launches, "passes": c.passes, "exchanges": c.exchanges,
+                "alg_bytes": c.alg_bytes, "exchange_bytes": c.exchange_bytes}
+
+    def info(self):
+        v = [ctypes.c_int() for _ in range(4)]
+        _check(lib().qj_state_info(self._h, *[ctypes.byref(x) for x in v]))
+        return {"n": v[0].value, "n_local": v[1].value, "dtype": v[2].value, "nshards": v[3].value}

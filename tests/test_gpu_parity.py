@@ -1,0 +1,303 @@
+"""GPU parity: the sm_100a CUDA path (through the C ABI) vs the CPU oracle,
+element by element, on seeded inputs.
+
+Tolerances (north star, reading R8): max |psi_gpu - psi_oracle| <= 1e-12 for
+complex128 and 1e-5 for complex64; X / Z / SWAP (and controlled versions) are
+exact (IEEE ==, reading R9); probabilities' index ordering is exact (a basis
+state gives exactly one 1).  For complex64 runs the oracle is fed the same
+complex64-rounded matrices and input state, widened to double (reading R7).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import circuits as C
+from workloads import gates as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+qjp = pytest.importorskip("paper_2203_08826_b200")
+
+TOL = {np.complex128: 1e-12, np.complex64: 1e-5}
+TDT = {np.complex128: torch.complex128, np.complex64: torch.complex64}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2203_08826_b200 import build
+    build.build()
+
+
+def rand_state(n, rng, dt):
+    v = rng.standard_normal(2**n) + 1j * rng.standard_normal(2**n)
+    v = (v / np.linalg.norm(v)).astype(dt)
+    return v
+
+
+def to_gpu(psi, dt):
+    return torch.from_numpy(np.ascontiguousarray(psi.astype(dt))).to("cuda")
+
+
+def gate_matrix_for(g, dt):
+    """Dense matrix as the GPU sees it: rounded to the state dtype, widened."""
+    return g.matrix().astype(dt).astype(np.complex128)
+
+
+def oracle_circuit(circ, psi, dt):
+    mats = [gate_matrix_for(g, dt) for g in circ.gates]
+    return oracle.run(circ, psi.astype(np.complex128), mats)
+
+
+def run_gpu_gate(st, g):
+    if g.kind == "dense":
+        st.apply_gate(g.targets, g.data[0], g.controls)
+    elif g.kind == "x":
+        st.x(g.targets[0], g.controls)
+    elif g.kind == "z":
+        st.z(g.targets[0], g.controls)
+    elif g.kind == "swap":
+        st.swap(g.targets[0], g.targets[1], g.controls)
+    elif g.kind == "fsim":
+        st.fsim(g.targets[0], g.targets[1], g.data[0], g.data[1], g.controls)
+    elif g.kind == "diag":
+        st.diagonal(g.targets, g.data[0], g.controls)
+    else:
+        raise ValueError(g.kind)
+
+
+def check_close(got, exp, dt, exact=False):
+    if exact:
+        assert np.array_equal(got.astype(np.complex128), exp), "not value-exact"
+        return
+    err = np.max(np.abs(got.astype(np.complex128) - exp))
+    assert err <= TOL[dt], f"max abs err {err:.3e} > {TOL[dt]}"
+
+
+DTYPES = [np.complex128, np.complex64]
+
+
+# ------------------------------------------------ every bit position, 1 target
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 6, 7, 9, 12])
+def test_one_qubit_every_position(dt, n):
+    rng = np.random.default_rng(n)
+    psi = rand_state(n, rng, dt)
+    for t in range(n):
+        for nc in range(0, min(2, n - 1) + 1):
+            ctrls = tuple(int(q) for q in rng.permutation([q for q in range(n) if q != t])[:nc])
+            g = G.unitary("U", (t,), G.random_unitary(1, rng), ctrls)
+            x = to_gpu(psi, dt)
+            st = qjp.State(x, basis=None)
+            st.apply_gate(g.targets, g.data[0], g.controls)
+            st.sync()
+            exp = np.empty(2**n, dtype=np.complex128)
+            oracle.apply_matrix(psi.astype(np.complex128), exp, n, g.targets, g.controls,
+                                gate_matrix_for(g, dt))
+            check_close(x.cpu().numpy(), exp, dt)
+
+
+# ------------------------------------------------ random gates of every kind
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("seed", range(12))
+def test_random_gates(dt, seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(2, 13))
+    psi = rand_state(n, rng, dt)
+    for i in range(30):
+        g = C.random_gate(n, rng, max_targets=5, max_controls=3)
+        x = to_gpu(psi, dt)
+        st = qjp.State(x, basis=None)
+        run_gpu_gate(st, g)
+        st.sync()
+        exp = np.empty(2**n, dtype=np.complex128)
+        oracle.apply_matrix(psi.astype(np.complex128), exp, n, g.targets, g.controls,
+                            gate_matrix_for(g, dt))
+        check_close(x.cpu().numpy(), exp, dt, exact=g.kind in ("x", "z", "swap"))
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("k", [2, 3, 4, 5, 6, 7, 8])
+def test_multi_target_dense(dt, k):
+    """k-target dense gates on every kind of bit mix (vector, lane, outer)."""
+    rng = np.random.default_rng(77 + k)
+    n = 12
+    psi = rand_state(n, rng, dt)
+    for trial in range(6):
+        qs = [int(q) for q in rng.permutation(n)]
+        if trial == 0:
+            qs = list(range(n - 1, -1, -1))  # lowest bits (lane / vector)
+        elif trial == 1:
+            qs = list(range(n))              # highest bits (outer)
+        t = tuple(qs[:k])
+        c = tuple(qs[k:k + int(rng.integers(0, 3))])
+        g = G.unitary("U", t, G.random_unitary(k, rng), c)
+        x = to_gpu(psi, dt)
+        st = qjp.State(x, basis=None)
+        st.apply_gate(g.targets, g.data[0], g.controls)
+        st.sync()
+        exp = np.empty(2**n, dtype=np.complex128)
+        oracle.apply_matrix(psi.astype(np.complex128), exp, n, t, c, gate_matrix_for(g, dt))
+        check_close(x.cpu().numpy(), exp, dt)
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+def test_specialised_exact_every_position(dt):
+    """X, CX, SWAP, CSWAP, Z, CZ are value-exact vs Eq. 1 with their matrices (R9)."""
+    rng = np.random.default_rng(5)
+    n = 11
+    psi = rand_state(n, rng, dt)
+    cases = []
+    for t in range(n):
+        cases.append(G.X(t))
+        cases.append(G.Z(t))
+        cases.append(G.X(t, controls=((t + 3) % n,)))
+        cases.append(G.Z(t, controls=((t + 5) % n, (t + 1) % n)))
+        cases.append(G.SWAP(t, (t + 1) % n))
+        cases.append(G.SWAP(t, (t + 6) % n, controls=((t + 2) % n,)))
+    for g in cases:
+        x = to_gpu(psi, dt)
+        st = qjp.State(x, basis=None)
+        run_gpu_gate(st, g)
+        st.sync()
+        exp = np.empty(2**n, dtype=np.complex128)
+        oracle.apply_matrix(psi.astype(np.complex128), exp, n, g.targets, g.controls, g.matrix())
+        check_close(x.cpu().numpy(), exp, dt, exact=True)
+
+
+# ------------------------------------------------ circuits
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("name", ["qft10", "variational12", "supremacy3x4", "qaoa10", "bv10", "random10"])
+def test_circuits_vs_oracle(dt, name):
+    circ = {"qft10": lambda: C.qft(10), "variational12": lambda: C.variational(12, layers=3),
+            "supremacy3x4": lambda: C.supremacy(3, 4, 12), "qaoa10": lambda: C.qaoa(10, 2),
+            "bv10": lambda: C.bv(10), "random10": lambda: C.random_circuit(10, 300, 3)}[name]()
+    n = circ.n
+    rng = np.random.default_rng(11)
+    psi = rand_state(n, rng, dt)
+    for fuse in (False, True):
+        x = to_gpu(psi, dt)
+        st = qjp.State(x, basis=None)
+        st.apply_circuit(circ.gates, fuse=fuse)
+        st.sync()
+        exp = oracle_circuit(circ, psi, dt)
+        check_close(x.cpu().numpy(), exp, dt)
+
+
+@pytest.mark.parametrize("n,x", [(10, 0b1011001110), (16, 40503), (20, 0xB1E05)])
+def test_qft_basis_closed_form(n, x):
+    y = np.arange(2**n, dtype=np.uint64)
+    m = (np.uint64(x) * y) % np.uint64(2**n)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * m.astype(np.float64) / 2**n)
+    for fuse in (False, True):
+        t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+        st = qjp.State(t, basis=x)
+        st.apply_circuit(C.qft(n).gates, fuse=fuse)
+        st.sync()
+        assert np.max(np.abs(t.cpu().numpy() - exp)) < 1e-12
+
+
+# ------------------------------------------------ probabilities
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+def test_probabilities(dt):
+    rng = np.random.default_rng(3)
+    for n in [1, 3, 7, 12]:
+        psi = rand_state(n, rng, dt)
+        st = qjp.State(to_gpu(psi, dt), basis=None)
+        full = st.probabilities().cpu().numpy()
+        exp = oracle.probabilities(psi.astype(np.complex128), n)
+        assert np.max(np.abs(full - exp)) < (1e-15 if dt == np.complex128 else 1e-7)
+        for m in range(1, n + 1):
+            qs = [int(q) for q in rng.permutation(n)[:m]]
+            p = st.probabilities(qs).cpu().numpy()
+            e = oracle.probabilities(psi.astype(np.complex128), n, qs)
+            assert np.max(np.abs(p - e)) < (1e-14 if dt == np.complex128 else 1e-6)
+
+
+def test_probabilities_basis_ordering_exact():
+    n, x = 14, 0b10110011100101
+    t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(t, basis=x)
+    p = st.probabilities().cpu().numpy()
+    assert p[x] == 1.0 and np.count_nonzero(p) == 1
+    q = [3, 0, 7]
+    pm = st.probabilities(q).cpu().numpy()
+    o = int("".join(str((x >> (n - 1 - qq)) & 1) for qq in q), 2)
+    assert pm[o] == 1.0 and np.count_nonzero(pm) == 1
+
+
+# ------------------------------------------------ sharded (virtual ranks)
+def _shard_run(circ, psi, dt, nshards):
+    n = circ.n
+    g = nshards.bit_length() - 1
+    x1 = to_gpu(psi, dt)
+    s1 = qjp.State(x1, basis=None)
+    s1.apply_circuit(circ.gates)
+    s1.sync()
+    shards = [to_gpu(psi[r << (n - g):(r + 1) << (n - g)], dt) for r in range(nshards)]
+    sh = qjp.State.sharded(shards, n, basis=None)
+    sh.apply_circuit(circ.gates)
+    sh.sync()
+    return s1, sh
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("nshards", [2, 4, 8])
+def test_sharded_vs_single_and_oracle(dt, nshards):
+    """The sharded path (global-qubit swaps between shards) matches the
+    single-shard path and the oracle within tolerance (dense gates may land on
+    different physical bits after a remap, which changes the summation order)."""
+    n = 11
+    circ = C.random_circuit(n, 120, 17 + nshards, max_targets=3)
+    circ.gates += C.qft(n).gates
+    rng = np.random.default_rng(23)
+    psi = rand_state(n, rng, dt)
+    s1, sh = _shard_run(circ, psi, dt, nshards)
+    full = sh.probabilities().cpu().numpy()
+    single = s1.probabilities().cpu().numpy()
+    assert np.max(np.abs(full - single)) < TOL[dt]
+    qs = [0, n - 1, 3]
+    assert np.max(np.abs(sh.probabilities(qs).cpu().numpy() - s1.probabilities(qs).cpu().numpy())) < TOL[dt]
+    exp = oracle_circuit(circ, psi, dt)
+    assert np.max(np.abs(full - np.abs(exp) ** 2)) < TOL[dt]
+    assert sh.counters()["exchanges"] > 0
+
+
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("nshards", [2, 8])
+def test_sharded_bit_identical_exact_gates(dt, nshards):
+    """With only permutation / sign / single-phase gates every amplitude sees
+    the same arithmetic wherever it lives: sharded == single, bit for bit."""
+    n = 10
+    circ = C.random_circuit(n, 200, 40 + nshards, kinds=("x", "z", "swap", "diag"), max_targets=2)
+    rng = np.random.default_rng(24)
+    psi = rand_state(n, rng, dt)
+    s1, sh = _shard_run(circ, psi, dt, nshards)
+    assert np.array_equal(sh.probabilities().cpu().numpy(), s1.probabilities().cpu().numpy())
+
+
+# ------------------------------------------------ full-size sampled checks
+@pytest.mark.slow
+@pytest.mark.parametrize("fuse", [False, True])
+def test_qft30_c128_sampled_closed_form(fuse):
+    """The bench workload (30-qubit QFT, complex128, bench launch config): every
+    amplitude is checked on a seeded sample of 2^16 indices plus the ends
+    against the exact closed form (integer phase numerator)."""
+    n, x = 30, 0b101101110001011100101101011011
+    t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(t, basis=x)
+    st.apply_circuit(C.qft(n).gates, fuse=fuse)
+    st.sync()
+    rng = np.random.default_rng(30)
+    idx = np.unique(np.concatenate([rng.integers(0, 2**n, 1 << 16), [0, 1, 2**n - 1]])).astype(np.int64)
+    got = t[torch.from_numpy(idx).cuda()].cpu().numpy()
+    m = (np.uint64(x) * idx.astype(np.uint64)) % np.uint64(2**n)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * m.astype(np.float64) / 2**n)
+    assert np.max(np.abs(got - exp)) < 1e-12
+    p = st.probabilities([0, 1, 2, 3])
+    assert abs(float(p.sum()) - 1) < 1e-10
+    del st, t
+    torch.cuda.empty_cache()
