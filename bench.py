@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py -- seconds per circuit and effective HBM GB/s of the hot path
+(BASELINE.json metric) on the 30-qubit complex128 QFT (BASELINE.json
+configs[2], the configuration the north-star target is quoted on).
+
+One step = one pass of the whole hot path over one synthetic input:
+    qj_state_reset(|x>)            (a1: state layout / init)
+    qj_apply_circuit(QFT30)        (a2-a6: every gate of the circuit)
+    qj_probabilities(10 qubits)    (a7: Born-rule marginal readout)
+Timed with CUDA events on the state's stream; the 16 GiB state is far larger
+than the 126 MB L2, so no flush is needed between steps.
+
+Arms:
+  default          the sm_100a library through the C ABI (paper_2203_08826_b200)
+  --impl reference the CPU oracle (oracle/, plain fp64 C/OpenMP Eq. 1) on the
+                   host cores: each step applies a bounded sample of the QFT30
+                   gates to a 2^30 state and extrapolates to s/circuit.
+
+Multi-GPU (torchrun, N>1): every rank runs its own QFT30 circuit (independent
+problems, weak scaling, no data-path collective); the max over ranks of the
+device time is used and value = that time / (steps * N).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QFT/random-circuit sec per circuit and effective HBM GB/s vs peak, 1/2/4/8 B200"
+SEED_X = 0b101101110001011100101101011011  # the seeded 30-bit basis input |x>
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """dram read+write bytes per launch from the committed ncu --set full capture."""
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
+            os.path.join(ROOT, "profiles")) else []:
+        if name.startswith("ncu_traffic") and name.endswith(".json"):
+            try:
+                with open(os.path.join(ROOT, "profiles", name)) as f:
+                    return json.load(f), name
+            except Exception:
+                pass
+    return {}, None
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception:
+                        pass
+                    time.sleep(0.05)
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=1)
+
+    def summary(self):
+        r = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": r, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- workloads
+def make_workload(name):
+    from workloads import circuits as C
+    if name == "qft30_c128":
+        return dict(n=30, dtype="c128", circ=C.qft(30), basis=SEED_X, readout=list(range(10)))
+    if name == "qft28_c128":
+        return dict(n=28, dtype="c128", circ=C.qft(28), basis=SEED_X & ((1 << 28) - 1), readout=list(range(10)))
+    if name == "var20_c128":
+        return dict(n=20, dtype="c128", circ=C.variational(20, layers=20), basis=0, readout=list(range(10)))
+    if name == "var20_c64":
+        return dict(n=20, dtype="c64", circ=C.variational(20, layers=20), basis=0, readout=list(range(10)))
+    if name == "sup32_c64":
+        return dict(n=32, dtype="c64", circ=C.supremacy(4, 8, 20), basis=0, readout=list(range(10)))
+    if name == "qft10_c128":
+        return dict(n=10, dtype="c128", circ=C.qft(10), basis=SEED_X & 1023, readout=list(range(10)))
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ----------------------------------------------------------------- oracle timing
+def oracle_sample(wl, reps=1):
+    """Time the CPU oracle on a bounded sample of the workload's gates applied
+    to a full 2^n state and extrapolate to seconds per circuit: one gate of each
+    (kind, #targets, #controls) class present in the circuit, weighted by the
+    class counts (the oracle's cost per gate depends only on that class)."""
+    import numpy as np
+    import oracle
+
+    n = wl["n"]
+    classes = {}
+    for g in wl["circ"].gates:
+        key = (len(g.targets), len(g.controls))
+        classes.setdefault(key, [g, 0])
+        classes[key][1] += 1
+    psi = oracle.basis_state(n, wl["basis"])
+    out = np.empty_like(psi)
+    total = 0.0
+    parts = []
+    for key, (g, cnt) in sorted(classes.items()):
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.apply_matrix(psi, out, n, g.targets, g.controls, g.matrix())
+        dt = (time.perf_counter() - t0) / reps
+        total += dt * cnt
+        parts.append(f"{cnt}x[{key[0]}t,{key[1]}c] {dt:.3f}s")
+    return total, "; ".join(parts), oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    wl = make_workload(args.workload)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sample, cores = oracle_sample(wl)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s/circuit",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "n": wl["n"], "gates": len(wl["circ"])},
+        "cpu_baseline": {"value": value, "unit": "s/circuit", "cores": cores, "kind": "oracle",
+                         "sample": f"one gate per class on a 2^{wl['n']} state, extrapolated by class "
+                                   f"counts: {sample}"},
+        "e2e": {"value": value, "unit": "s/circuit", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- qj arm
+def run_qj(args, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2203_08826_b200 as qj
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    wl = make_workload(args.workload)
+    n = wl["n"]
+    tdt = torch.complex128 if wl["dtype"] == "c128" else torch.complex64
+    amp_bytes = 16 if wl["dtype"] == "c128" else 8
+    t_load0 = time.perf_counter()
+    qj.lib()
+    stream = torch.cuda.Stream(dev)
+    psi = torch.empty(1 << n, dtype=tdt, device=dev)
+    st = qj.State(psi, basis=None, stream=stream)
+    gates = wl["circ"].gates
+    packed = st.pack_circuit(gates)
+    readout = wl["readout"]
+    pbuf = torch.empty(1 << len(readout), dtype=st.real_dtype, device=dev)
+
+    def step():
+        st.reset(wl["basis"])
+        st.apply_circuit(None, fuse=args.fuse, packed=packed)
+        st.probabilities(readout, out=pbuf)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+
+    # dry run: first circuit after library load
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        step()
+        ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dry_run_s = ev0.elapsed_time(ev1) / 1e3
+    load_s = time.perf_counter() - t_load0
+    for _ in range(max(0, args.warmup - 1)):
+        step()
+    barrier()
+
+    # ---- timed region (device events, per-pass profiling events on) ----
+    st.counters(reset=True)
+    st.set_profiling(True)
+    st.profile(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    prof = st.profile(reset=True)
+    st.set_profiling(False)
+    ctr = st.counters(reset=True)
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+
+    # ---- e2e: the public API with host buffers each step ----
+    host_out = torch.empty(1 << len(readout), dtype=st.real_dtype, pin_memory=True)
+    h2d = 0
+    for g in gates:
+        h2d += 112  # sizeof(qj_gate)
+        if g.kind in ("dense", "diag", "fsim"):
+            cnt = {"dense": 4 ** len(g.targets), "diag": 2 ** len(g.targets), "fsim": 5}[g.kind]
+            h2d += cnt * amp_bytes
+    d2h = host_out.numel() * host_out.element_size()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        st.reset(wl["basis"])
+        st.apply_circuit(gates, fuse=args.fuse)           # packs host gate list each step
+        p = st.probabilities(readout, out=pbuf)
+        with torch.cuda.stream(stream):
+            host_out.copy_(p, non_blocking=True)
+        stream.synchronize()
+    f1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- parity spot check of the benched state (not timed) ----
+    check = None
+    if args.workload.startswith("qft"):
+        rng = np.random.default_rng(30)
+        idx = np.unique(np.concatenate([rng.integers(0, 1 << n, 4096), [0, (1 << n) - 1]])).astype(np.int64)
+        got = psi[torch.from_numpy(idx).to(dev)].cpu().numpy()
+        m = (np.uint64(wl["basis"]) * idx.astype(np.uint64)) % np.uint64(1 << n)
+        exp = 2 ** (-n / 2) * np.exp(2j * np.pi * m.astype(np.float64) / (1 << n))
+        check = float(np.max(np.abs(got - exp)))
+
+    if rank != 0:
+        return 0
+    steps = args.steps
+    value = ms_max / 1e3 / (steps * world)
+    per_step_bytes = ctr["alg_bytes"] / steps
+    peak, peak_src = load_peaks()
+    traffic, traffic_src = load_traffic()
+    dom = max(prof.items(), key=lambda kv: kv[1]["total_ms"]) if prof else (None, None)
+    roof = None
+    if dom[0]:
+        k, d = dom
+        ach = d["alg_bytes"] / (d["total_ms"] / 1e3) / 1e9
+        per_launch = d["alg_bytes"] / d["launches"]
+        tr = traffic.get(k) if traffic else None
+        roof = {"bound": "hbm", "kernel": k, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "peak_source": peak_src,
+                "alg_bytes_per_launch": per_launch,
+                "avg_launch_us": d["total_ms"] / d["launches"] * 1e3,
+                "share_of_step": d["total_ms"] / max(ms, 1e-9),
+                "traffic": (tr["dram_bytes_per_launch"] if tr else None),
+                "traffic_source": traffic_src}
+    kinds = {k: {"launches_per_step": v["launches"] / steps, "ms_per_step": v["total_ms"] / steps,
+                 "GBps": v["alg_bytes"] / max(v["total_ms"], 1e-12) / 1e6,
+                 "frac": v["alg_bytes"] / max(v["total_ms"], 1e-12) / 1e6 / peak}
+             for k, v in prof.items()}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, sample, cores = oracle_sample(wl)
+        cpu = {"value": v, "unit": "s/circuit", "cores": cores, "kind": "oracle",
+               "sample": f"one gate per class on a 2^{n} state, extrapolated by class counts: {sample}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "s/circuit", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / steps, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if wl["dtype"] == "c128" else "f32",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "n": n, "state": wl["dtype"], "gates": len(gates),
+                   "basis": wl["basis"], "fuse": bool(args.fuse),
+                   "step": "state_reset + apply_circuit + 10-qubit marginal probabilities",
+                   "l2": f"state {amp_bytes << n >> 20} MiB >> 126 MB L2: inputs larger than L2, no flush",
+                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU"},
+        "effective_gbs": per_step_bytes / (ms_max / steps / 1e3) / 1e9,
+        "effective_frac": per_step_bytes / (ms_max / steps / 1e3) / 1e9 / peak,
+        "alg_bytes_per_step": per_step_bytes,
+        "roofline": roof,
+        "kinds": kinds,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_ms / 1e3 / (steps * world), "unit": "s/circuit",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": ctr["launches"],
+        "clocks": clk.summary(),
+        "dry_run_s": dry_run_s, "first_call_incl_load_s": load_s,
+        "parity_max_abs_err_sampled": check,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="qj", choices=["qj", "reference"])
+    ap.add_argument("--workload", default="qft30_c128")
+    ap.add_argument("--fuse", dest="fuse", action="store_true", default=False)
+    ap.add_argument("--no-fuse", dest="fuse", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        torch.distributed.init_process_group("nccl")
+    try:
+        return run_qj(args, rank, world)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -178,6 +178,23 @@ typedef struct {
 
 qj_status qj_get_counters(qj_state s, qj_counters* out, int reset);
 
+/* Per-kernel-kind timing: with profiling on, the library records a pair of
+ * CUDA events on the handle's stream around every pass it enqueues.
+ * qj_get_profile synchronises the stream and returns, per pass kind
+ * ("gate_dense", "gate_x", "gate_swap", "diag_table", "diag_phase",
+ * "diag_neg", "tile", "exchange"), the number of launches, their summed
+ * device time and their summed algorithmic bytes.  `count` receives the
+ * number of entries written (<= max_entries). */
+typedef struct {
+    char name[32];
+    uint64_t launches;
+    double total_ms;
+    double alg_bytes;
+} qj_profile_entry;
+
+qj_status qj_set_profiling(qj_state s, int on);
+qj_status qj_get_profile(qj_state s, qj_profile_entry* out, int max_entries, int* count, int reset);
+
 /* n, local qubits, dtype, number of shards of the handle. */
 qj_status qj_state_info(qj_state s, int* n, int* n_local, int* dtype, int* nshards);
 

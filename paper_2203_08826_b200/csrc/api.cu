@@ -51,7 +51,20 @@ struct qj_state_s {
     LaunchStats ls;
     qj_counters ctr{};
     Planner planner;
+    // profiling: event pairs around passes
+    bool profiling = false;
+    struct Rec {
+        int kind;
+        double bytes;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
 };
+
+static const char* kProfNames[] = {"gate_dense", "gate_x",     "gate_swap", "diag_table",
+                                   "diag_phase", "diag_neg",   "tile",      "exchange"};
+enum { PROF_TILE = 6, PROF_EXCHANGE = 7, PROF_N = 8 };
 
 namespace {
 
@@ -164,11 +177,42 @@ qj_status make_lgate(qj_state s, int kind, const int* targets, int nt, const int
     return QJ_OK;
 }
 
+cudaEvent_t pool_get(qj_state s) {
+    if (!s->pool.empty()) {
+        cudaEvent_t e = s->pool.back();
+        s->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    qj_state s;
+    int kind;
+    double bytes;
+    cudaEvent_t a = nullptr;
+    ProfScope(qj_state s_, int kind_, double bytes_) : s(s_), kind(kind_), bytes(bytes_) {
+        if (!s->profiling) return;
+        a = pool_get(s);
+        cudaEventRecord(a, s->stream);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEvent_t b = pool_get(s);
+        cudaEventRecord(b, s->stream);
+        s->recs.push_back({kind, bytes, a, b});
+    }
+};
+
 // Execute planned steps on the device.
 qj_status execute(qj_state s, const std::vector<Step>& steps) {
     cudaError_t e = cudaSuccess;
     for (const Step& st : steps) {
         if (st.type == Step::EXCHANGE) {
+            const double xb = (double)s->amp_bytes * (double)(1ull << (s->nl - 1)) * (double)s->shards.size();
+            ProfScope prof(s, PROF_EXCHANGE, xb);
             // swap global bit (nl + j) with local bit L: pair shards r (bit j = 0) and r | 1<<j
             const int j = st.gbit, L = st.lbit;
             for (size_t r = 0; r < s->shards.size(); ++r) {
@@ -181,13 +225,14 @@ qj_status execute(qj_state s, const std::vector<Step>& steps) {
                 if (e != cudaSuccess) return cuda_fail(e, "exchange launch");
             }
             s->ctr.exchanges++;
-            s->ctr.exchange_bytes += (double)s->amp_bytes * (double)(1ull << s->nl) * (double)s->shards.size();
+            s->ctr.exchange_bytes += xb;
             continue;
         }
         if (st.pass.k > 5 && st.pass.kind == PK_DENSE) {
             const size_t need = (size_t)s->amp_bytes * ((size_t)1 << (2 * st.pass.k));
             if (qj_status q = ensure_scratch(s, need)) return q;
         }
+        ProfScope prof(s, st.type == Step::TILE ? PROF_TILE : st.pass.kind, st.alg_bytes);
         e = by_dtype(s->dt, [&](auto z) {
             using R = decltype(z);
             if (st.type == Step::TILE) return run_tile<R>(st.tile, s->shards[st.shard], s->nl, s->stream, s->ls);
@@ -295,9 +340,54 @@ qj_status qj_state_reset(qj_state s, uint64_t basis_index) {
     return QJ_OK;
 }
 
+qj_status qj_set_profiling(qj_state s, int on) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    s->profiling = on != 0;
+    return QJ_OK;
+}
+
+qj_status qj_get_profile(qj_state s, qj_profile_entry* out, int max_entries, int* count, int reset) {
+    if (!s || !count || (max_entries > 0 && !out)) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
+    cudaError_t e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "qj_get_profile");
+    uint64_t launches[PROF_N] = {};
+    double ms[PROF_N] = {}, bytes[PROF_N] = {};
+    for (auto& r : s->recs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        launches[r.kind]++;
+        ms[r.kind] += t;
+        bytes[r.kind] += r.bytes;
+    }
+    int c = 0;
+    for (int k = 0; k < PROF_N && c < max_entries; ++k) {
+        if (!launches[k]) continue;
+        std::memset(&out[c], 0, sizeof(out[c]));
+        std::strncpy(out[c].name, kProfNames[k], sizeof(out[c].name) - 1);
+        out[c].launches = launches[k];
+        out[c].total_ms = ms[k];
+        out[c].alg_bytes = bytes[k];
+        ++c;
+    }
+    *count = c;
+    if (reset) {
+        for (auto& r : s->recs) {
+            s->pool.push_back(r.a);
+            s->pool.push_back(r.b);
+        }
+        s->recs.clear();
+    }
+    return QJ_OK;
+}
+
 qj_status qj_state_free(qj_state s) {
     if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
-    if (s->scratch || s->bins) cudaStreamSynchronize(s->stream);
+    cudaStreamSynchronize(s->stream);
+    for (auto& r : s->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto ev : s->pool) cudaEventDestroy(ev);
     if (s->scratch) cudaFree(s->scratch);
     if (s->bins) cudaFree(s->bins);
     delete s;

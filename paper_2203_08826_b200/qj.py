@@ -29,7 +29,7 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_apply_gate", "qj_apply_x", "qj_apply_z", "qj_apply_swap", "qj_apply_fsim",
            "qj_apply_diagonal", "qj_apply_circuit", "qj_probabilities", "qj_sync",
            "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
-           "qj_insert_zero_bits"]
+           "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile"]
 
 
 class QJError(RuntimeError):
@@ -49,6 +49,11 @@ class qj_counters(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_uint64), ("passes", ctypes.c_uint64),
                 ("exchanges", ctypes.c_uint64), ("alg_bytes", ctypes.c_double),
                 ("exchange_bytes", ctypes.c_double)]
+
+
+class qj_profile_entry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64),
+                ("total_ms", ctypes.c_double), ("alg_bytes", ctypes.c_double)]
 
 
 _lib = None
@@ -83,6 +88,8 @@ def lib():
         "qj_last_error": ([], ctypes.c_char_p),
         "qj_version": ([], ctypes.c_char_p),
         "qj_insert_zero_bits": ([U64, IP, I], U64),
+        "qj_set_profiling": ([P, I], S),
+        "qj_get_profile": ([P, ctypes.POINTER(qj_profile_entry), I, IP, I], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -264,6 +271,18 @@ class State:
         _check(lib().qj_get_counters(self._h, ctypes.byref(c), 1 if reset else 0))
         return {"launches": c.launches, "passes": c.passes, "exchanges": c.exchanges,
                 "alg_bytes": c.alg_bytes, "exchange_bytes": c.exchange_bytes}
+
+    def set_profiling(self, on=True):
+        _check(lib().qj_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self, reset=True):
+        """{kind: {"launches", "total_ms", "alg_bytes"}} of the passes enqueued
+        while profiling was on (synchronises the stream)."""
+        arr = (qj_profile_entry * 16)()
+        cnt = ctypes.c_int()
+        _check(lib().qj_get_profile(self._h, arr, 16, ctypes.byref(cnt), 1 if reset else 0))
+        return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
+                                       "alg_bytes": arr[i].alg_bytes} for i in range(cnt.value)}
 
     def info(self):
         v = [ctypes.c_int() for _ in range(4)]
