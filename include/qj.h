@@ -154,6 +154,16 @@ typedef struct {
  * before anything is enqueued. */
 qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_t flags);
 
+/* Physical layout.  Qubit labels at this ABI are always logical: the handle
+ * tracks a logical->physical bit map.  Fused circuits apply uncontrolled SWAP
+ * gates as relabellings of that map and sharded states remap global qubits,
+ * so after qj_apply_circuit(QJ_FUSE) or on sharded states the amplitude
+ * buffer may hold the state in a permuted bit order (qj_probabilities is
+ * canonical regardless).  qj_state_canonicalize moves the data back to the
+ * canonical order (R1) with SWAP passes / exchanges and resets the map.
+ * Errors: UNSUPPORTED if two global bits would have to trade places. */
+qj_status qj_state_canonicalize(qj_state s);
+
 /* ---- readout -----------------------------------------------------------------
  * Born-rule probabilities.  qubits == NULL and nq == -1:
  * the full vector |psi_i|^2 in canonical index order (2^n values).  Otherwise

@@ -51,6 +51,7 @@ struct qj_state_s {
     LaunchStats ls;
     qj_counters ctr{};
     Planner planner;
+    TileStaging stg;  // tile-pass program buffers
     // profiling: event pairs around passes
     bool profiling = false;
     struct Rec {
@@ -235,7 +236,8 @@ qj_status execute(qj_state s, const std::vector<Step>& steps) {
         ProfScope prof(s, st.type == Step::TILE ? PROF_TILE : st.pass.kind, st.alg_bytes);
         e = by_dtype(s->dt, [&](auto z) {
             using R = decltype(z);
-            if (st.type == Step::TILE) return run_tile<R>(st.tile, s->shards[st.shard], s->nl, s->stream, s->ls);
+            if (st.type == Step::TILE)
+                return run_tile<R>(st.tile, s->shards[st.shard], s->nl, s->stream, s->stg, s->ls);
             return run_pass<R>(st.pass, s->shards[st.shard], s->nl, s->stream, s->scratch, s->scratch_bytes, s->ls);
         });
         if (e != cudaSuccess) return cuda_fail(e, "pass launch");
@@ -388,6 +390,7 @@ qj_status qj_state_free(qj_state s) {
         cudaEventDestroy(r.b);
     }
     for (auto ev : s->pool) cudaEventDestroy(ev);
+    s->stg.release();
     if (s->scratch) cudaFree(s->scratch);
     if (s->bins) cudaFree(s->bins);
     delete s;
@@ -546,6 +549,45 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
     if (e != cudaSuccess) return cuda_fail(e, "bins launch");
     s->ctr.launches = s->ls.launches;
     return QJ_OK;
+}
+
+qj_status qj_state_canonicalize(qj_state s) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    const int n = s->n, nl = s->nl;
+    std::vector<int> phys = s->phys;
+    std::vector<Step> steps;
+    for (int q = 0; q < n; ++q) {
+        const int want = n - 1 - q, cur = phys[q];
+        if (cur == want) continue;
+        int q2 = 0;
+        while (phys[q2] != want) ++q2;
+        if (cur < nl && want < nl) {
+            for (size_t r = 0; r < s->shards.size(); ++r) {
+                Step st;
+                st.type = Step::PASS;
+                st.shard = (int)r;
+                st.pass.kind = PK_SWAP;
+                st.pass.k = 2;
+                st.pass.tpos[0] = cur;
+                st.pass.tpos[1] = want;
+                st.alg_bytes = pass_alg_bytes(st.pass, nl, s->amp_bytes);
+                steps.push_back(std::move(st));
+            }
+        } else if (cur >= nl && want >= nl) {
+            return fail(QJ_ERR_UNSUPPORTED, "canonicalize: global bits %d and %d would have to trade places", cur, want);
+        } else {
+            Step st;
+            st.type = Step::EXCHANGE;
+            st.gbit = std::max(cur, want) - nl;
+            st.lbit = std::min(cur, want);
+            steps.push_back(std::move(st));
+        }
+        phys[q] = want;
+        phys[q2] = cur;
+    }
+    qj_status st = execute(s, steps);
+    if (st == QJ_OK) s->phys = phys;
+    return st;
 }
 
 qj_status qj_sync(qj_state s) {

@@ -73,6 +73,15 @@ __device__ __forceinline__ void store_amp(void* psi, uint64_t idx, Cx<float> o) 
     __stcs(reinterpret_cast<float2*>(psi) + idx, make_float2(o.re, o.im));
 }
 
+__device__ __forceinline__ Cx<double> load_amp(const Cx<double>* psi, uint64_t idx) {
+    const double2 v = __ldcs(reinterpret_cast<const double2*>(psi) + idx);
+    return Cx<double>{v.x, v.y};
+}
+__device__ __forceinline__ Cx<float> load_amp(const Cx<float>* psi, uint64_t idx) {
+    const float2 v = __ldcs(reinterpret_cast<const float2*>(psi) + idx);
+    return Cx<float>{v.x, v.y};
+}
+
 template <typename R>
 __device__ __forceinline__ Cx<R> shfl_xor(Cx<R> v, int m) {
     return Cx<R>{__shfl_xor_sync(0xffffffffu, v.re, m), __shfl_xor_sync(0xffffffffu, v.im, m)};

@@ -186,8 +186,4 @@ void Planner::plan(const PlanContext& ctx, const std::vector<LGate>& gates, bool
     for (const LGate& g : gates) plan_gate(ctx, g, out);
 }
 
-void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates, std::vector<Step>& out) {
-    for (const LGate& g : gates) plan_gate(ctx, g, out);  // TODO(tile pass)
-}
-
 }  // namespace qj

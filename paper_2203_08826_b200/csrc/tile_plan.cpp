@@ -1,0 +1,329 @@
+// tile_plan.cpp -- fused planning (QJ_FUSE): pack consecutive gates into
+// window tile passes (tile.h), one HBM round trip per pass.
+//
+// Rules ("tile pass"):
+//  * an uncontrolled SWAP is a relabelling of two physical bits (the handle's
+//    logical->physical map; readout stays canonical through the map);
+//  * a diagonal gate (<= 3 targets) becomes phase terms on any bits -- it never
+//    widens the window;
+//  * a 1- or 2-target non-diagonal gate must have its targets in the window;
+//    the window grows (up to TILE_W bits, always including the low L bits that
+//    make 128-byte contiguous runs) until a gate does not fit, which closes
+//    the pass;
+//  * anything else (>= 3-target non-diagonal, > 3-target diagonal) closes the
+//    pass and runs as a single-gate pass.
+// Inside a pass, gates are split into segments of 4 register bits; diagonal
+// terms are deferred (they commute with every gate not targeting their bits)
+// and flushed into a RUN just before the first gate that targets one of their
+// bits, or at the end of the pass.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "planner.h"
+
+namespace qj {
+
+namespace {
+
+constexpr int kMaxOpsPerPass = TILE_MAXOPS - 16;
+constexpr int kMaxMatPerPass = TILE_MAXMAT;
+
+int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+bool is_diag(const std::vector<cd>& m, int D) {
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c)
+            if (r != c && m[(size_t)r * D + c] != cd(0, 0)) return false;
+    return true;
+}
+
+struct Item {
+    bool diag = false;
+    std::vector<HTerm> terms;  // diag
+    HOp op;                    // non-diag
+    uint64_t tmask = 0;        // non-diag target bits
+};
+
+struct PassBuild {
+    std::vector<Item> items;
+    std::vector<Step> singles;  // each gate as a single-gate pass, converted at admission
+    uint64_t W = 0;
+    int nops = 0, nmat = 0, nterms = 0, nnd = 0;  // nnd: non-diagonal ops (each may flush one run)
+};
+
+// Phase terms of a diagonal gate on physical positions.
+bool diag_terms(const LGate& g, const std::vector<int>& phys, std::vector<HTerm>& out) {
+    std::vector<cd> d;
+    const int k = g.nt;
+    if (g.kind == QJ_GATE_Z) {
+        d = {cd(1, 0), cd(-1, 0)};
+    } else if (g.kind == QJ_GATE_DIAG) {
+        d = g.data;
+    } else if (g.kind == QJ_GATE_DENSE && is_diag(g.data, 1 << k)) {
+        d.resize((size_t)1 << k);
+        for (int i = 0; i < (1 << k); ++i) d[i] = g.data[(size_t)i * (1 << k) + i];
+    } else {
+        return false;
+    }
+    if (k > 3) return false;
+    uint64_t cm = 0;
+    for (int i = 0; i < g.nc; ++i) cm |= 1ull << phys[g.c[i]];
+    for (int e = 0; e < (1 << k); ++e) {
+        if (d[e] == cd(1, 0)) continue;
+        HTerm t;
+        t.mask = cm;
+        t.val = cm;
+        for (int i = 0; i < k; ++i) {
+            const uint64_t b = 1ull << phys[g.t[i]];
+            t.mask |= b;
+            if ((e >> (k - 1 - i)) & 1) t.val |= b;
+        }
+        t.f = d[e];
+        out.push_back(t);
+    }
+    return true;
+}
+
+// Non-diagonal 1q/2q gate as a tile op.
+bool make_op(const LGate& g, const std::vector<int>& phys, HOp& op) {
+    if (g.nt > 2) return false;
+    op = HOp();
+    for (int i = 0; i < g.nc; ++i) op.cmask |= 1ull << phys[g.c[i]];
+    for (int i = 0; i < g.nt; ++i) op.t[i] = phys[g.t[i]];
+    switch (g.kind) {
+        case QJ_GATE_X:
+            op.type = TO_X;
+            return true;
+        case QJ_GATE_SWAP:
+            op.type = TO_SWAP;
+            return true;
+        case QJ_GATE_FSIM:
+            op.type = TO_U2;
+            op.m.assign(16, cd(0, 0));
+            op.m[0] = 1;
+            op.m[5] = g.data[0];
+            op.m[6] = g.data[1];
+            op.m[9] = g.data[2];
+            op.m[10] = g.data[3];
+            op.m[15] = g.data[4];
+            return true;
+        case QJ_GATE_DENSE:
+            op.type = g.nt == 1 ? TO_U1 : TO_U2;
+            op.m = g.data;
+            return true;
+        default:
+            return false;
+    }
+}
+
+// Choose the thread-bit order of a segment: lanes 0..C-1 on window bits of
+// distinct residues mod C (conflict-free swizzled SMEM), low bits first when
+// the segment touches HBM.
+void thread_bits(uint32_t rsel, int C, bool global, int8_t* tb) {
+    std::vector<int> avail;
+    for (int j = 0; j < TILE_W; ++j)
+        if (!((rsel >> j) & 1)) avail.push_back(j);
+    std::vector<int> order;
+    auto take = [&](int j) {
+        order.push_back(j);
+        avail.erase(std::find(avail.begin(), avail.end(), j));
+    };
+    if (global) {
+        for (int j = 0; j < C; ++j) take(j);  // low window bits on lanes 0..C-1
+    } else {
+        for (int res = 0; res < C; ++res) {
+            for (int j : avail)
+                if (j % C == res) {
+                    take(j);
+                    break;
+                }
+        }
+    }
+    for (int j : std::vector<int>(avail)) take(j);
+    for (int i = 0; i < TILE_T; ++i) tb[i] = (int8_t)order[i];
+}
+
+}  // namespace
+
+// Build the TileSpec of one pass.
+static bool build_tile(const PassBuild& pb, int nl, int C, TileSpec& ts) {
+    // window: pad to TILE_W bits with the highest unused local bits
+    uint64_t W = pb.W;
+    for (int b = nl - 1; b >= 0 && popc(W) < TILE_W; --b) W |= 1ull << b;
+    if (popc(W) != TILE_W) return false;
+    ts = TileSpec();
+    ts.w = TILE_W;
+    int loc[64];
+    for (int b = 0, j = 0; b < 64; ++b) {
+        loc[b] = -1;
+        if ((W >> b) & 1) {
+            ts.wpos[j] = b;
+            loc[b] = j++;
+        }
+    }
+    const uint32_t lowsel = (1u << C) - 1u;  // window-local low bits (the HBM runs)
+    struct SegB {
+        uint32_t rsel = 0;  // window-local register bits
+        std::vector<HOp> ops;
+    };
+    std::vector<SegB> segs(1);
+    std::vector<HTerm> pending;
+    auto flush = [&](uint64_t conflict_mask, bool all) {
+        HOp run;
+        run.type = TO_RUN;
+        std::vector<HTerm> keep;
+        for (auto& t : pending) {
+            if (all || (t.mask & conflict_mask)) run.terms.push_back(t);
+            else keep.push_back(t);
+        }
+        pending.swap(keep);
+        if (!run.terms.empty()) segs.back().ops.push_back(std::move(run));
+    };
+    for (const Item& it : pb.items) {
+        if (it.diag) {
+            pending.insert(pending.end(), it.terms.begin(), it.terms.end());
+            continue;
+        }
+        uint32_t tsel = 0;
+        for (int i = 0; i < (it.op.type == TO_U1 || it.op.type == TO_X ? 1 : 2); ++i) tsel |= 1u << loc[it.op.t[i]];
+        SegB& cur = segs.back();
+        const bool first = segs.size() == 1;
+        if ((tsel & ~cur.rsel) != 0) {
+            const uint32_t want = cur.rsel | tsel;
+            const bool fits = popc(want) <= TILE_R && !(first && (want & lowsel));
+            if (fits) {
+                cur.rsel = want;
+            } else {
+                segs.emplace_back();
+                segs.back().rsel = tsel;
+            }
+        }
+        flush(it.tmask, false);
+        segs.back().ops.push_back(it.op);
+    }
+    flush(0, true);
+    // the first and last segments touch HBM: their register bits must avoid the low bits
+    if (segs.front().rsel & lowsel) segs.insert(segs.begin(), SegB());
+    if (segs.back().rsel & lowsel) segs.emplace_back();
+    if ((int)segs.size() > TILE_MAXSEG) return false;
+    // pad register sets to TILE_R bits (prefer high window bits)
+    for (size_t s = 0; s < segs.size(); ++s) {
+        const bool global = (s == 0 || s + 1 == segs.size());
+        for (int j = TILE_W - 1; j >= 0 && popc(segs[s].rsel) < TILE_R; --j) {
+            if (global && ((lowsel >> j) & 1)) continue;
+            segs[s].rsel |= 1u << j;
+        }
+    }
+    for (size_t s = 0; s < segs.size(); ++s) {
+        TSeg S;
+        std::memset(&S, 0, sizeof(S));
+        const bool global = (s == 0 || s + 1 == segs.size());
+        for (int j = 0, k = 0; j < TILE_W; ++j)
+            if ((segs[s].rsel >> j) & 1) S.rbits[k++] = (int8_t)j;
+        thread_bits(segs[s].rsel, C, global, S.tbits);
+        S.op0 = (uint16_t)ts.ops.size();
+        for (auto& op : segs[s].ops) ts.ops.push_back(op);
+        S.op1 = (uint16_t)ts.ops.size();
+        ts.segs.push_back(S);
+    }
+    return (int)ts.ops.size() <= TILE_MAXOPS;
+}
+
+void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates, std::vector<Step>& out) {
+    if (ctx.g > 0 || ctx.nl < TILE_W + 2) {
+        for (const LGate& g : gates) plan_gate(ctx, g, out);
+        return;
+    }
+    std::vector<int>& phys = *ctx.phys;
+    const int C = ctx.amp_bytes == 16 ? 3 : 4;  // 128-byte runs: 8 x c128 / 16 x c64
+    const uint64_t low = (1ull << C) - 1ull;
+    const int max_terms = TILE_MAXTERMS;
+    PassBuild pb;
+    pb.W = low;
+    auto close = [&]() {
+        if (pb.items.empty()) return;
+        if (pb.singles.size() == 1) {
+            // a single gate: the specialised single-gate pass touches fewer bytes
+            if (pb.singles[0].shard >= 0) out.push_back(pb.singles[0]);
+        } else {
+            Step s;
+            s.type = Step::TILE;
+            s.shard = 0;
+            if (build_tile(pb, ctx.nl, C, s.tile) && tile_fits(s.tile, ctx.nl, ctx.amp_bytes)) {
+                s.alg_bytes = 2.0 * ctx.amp_bytes * std::ldexp(1.0, ctx.nl);
+                if (getenv("QJ_DEBUG_PLAN")) {
+                    int nruns = 0, nterms = 0;
+                    for (auto& op : s.tile.ops)
+                        if (op.type == TO_RUN) {
+                            ++nruns;
+                            nterms += (int)op.terms.size();
+                        }
+                    fprintf(stderr, "[qj plan] tile pass: %zu gates, window", pb.singles.size());
+                    for (int j = 0; j < TILE_W; ++j) fprintf(stderr, " %d", s.tile.wpos[j]);
+                    fprintf(stderr, " | %zu segs, %zu ops, %d runs, %d terms\n", s.tile.segs.size(),
+                            s.tile.ops.size(), nruns, nterms);
+                }
+                out.push_back(std::move(s));
+            } else {
+                // cannot happen with the limits below; stay correct anyway
+                for (const Step& st : pb.singles)
+                    if (st.shard >= 0) out.push_back(st);
+            }
+        }
+        pb = PassBuild();
+        pb.W = low;
+    };
+    auto single = [&](const LGate& g) {
+        Step s;
+        s.type = Step::PASS;
+        s.shard = 0;
+        if (!specialise(ctx, g, 0, s.pass)) s.shard = -1;  // identity
+        else s.alg_bytes = pass_alg_bytes(s.pass, ctx.nl, ctx.amp_bytes);
+        return s;
+    };
+    for (const LGate& g : gates) {
+        if (g.kind == QJ_GATE_SWAP && g.nc == 0) {
+            // relabel: the two logical qubits exchange physical bits
+            const int a = g.t[0], b = g.t[1];
+            std::swap(phys[a], phys[b]);
+            continue;
+        }
+        Item it;
+        std::vector<HTerm> terms;
+        if (diag_terms(g, phys, terms)) {
+            it.diag = true;
+            it.terms = std::move(terms);
+            if (pb.nterms + (int)it.terms.size() > max_terms - 8) close();
+            pb.nterms += (int)it.terms.size();
+            pb.items.push_back(std::move(it));
+            pb.singles.push_back(single(g));
+            continue;
+        }
+        HOp op;
+        if (!make_op(g, phys, op)) {
+            close();
+            plan_gate(ctx, g, out);
+            continue;
+        }
+        uint64_t tm = 0;
+        for (int i = 0; i < g.nt; ++i) tm |= 1ull << op.t[i];
+        const int nm = (int)op.m.size();
+        const bool fits = popc(pb.W | tm) <= TILE_W && pb.nops + 2 <= kMaxOpsPerPass &&
+                          pb.nmat + nm <= kMaxMatPerPass && pb.nnd + 1 < TILE_MAXRUNS;
+        if (!fits) close();
+        pb.W |= tm;
+        pb.nops += 2;  // the op plus a possible run flush before it
+        pb.nnd += 1;
+        pb.nmat += nm;
+        it.op = std::move(op);
+        it.tmask = tm;
+        pb.items.push_back(std::move(it));
+        pb.singles.push_back(single(g));
+    }
+    close();
+}
+
+}  // namespace qj

@@ -29,7 +29,7 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_apply_gate", "qj_apply_x", "qj_apply_z", "qj_apply_swap", "qj_apply_fsim",
            "qj_apply_diagonal", "qj_apply_circuit", "qj_probabilities", "qj_sync",
            "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
-           "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile"]
+           "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize"]
 
 
 class QJError(RuntimeError):
@@ -90,6 +90,7 @@ def lib():
         "qj_insert_zero_bits": ([U64, IP, I], U64),
         "qj_set_profiling": ([P, I], S),
         "qj_get_profile": ([P, ctypes.POINTER(qj_profile_entry), I, IP, I], S),
+        "qj_state_canonicalize": ([P], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -171,6 +172,11 @@ class State:
 
     def reset(self, basis=0):
         _check(lib().qj_state_reset(self._h, ctypes.c_uint64(QJ_KEEP if basis is None else basis)))
+
+    def canonicalize(self):
+        """Move the amplitudes back to canonical bit order (after fused circuits
+        relabelled SWAPs or sharded remaps); probabilities never need this."""
+        _check(lib().qj_state_canonicalize(self._h))
 
     def sync(self):
         _check(lib().qj_sync(self._h))

@@ -182,8 +182,12 @@ def test_circuits_vs_oracle(dt, name):
         x = to_gpu(psi, dt)
         st = qjp.State(x, basis=None)
         st.apply_circuit(circ.gates, fuse=fuse)
+        pf = st.probabilities([0, n - 1]).cpu().numpy()  # canonical through the map
+        st.canonicalize()
         st.sync()
         exp = oracle_circuit(circ, psi, dt)
+        pe = oracle.probabilities(exp, n, [0, n - 1])
+        assert np.max(np.abs(pf - pe)) < TOL[dt]
         check_close(x.cpu().numpy(), exp, dt)
 
 
@@ -196,6 +200,7 @@ def test_qft_basis_closed_form(n, x):
         t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
         st = qjp.State(t, basis=x)
         st.apply_circuit(C.qft(n).gates, fuse=fuse)
+        st.canonicalize()
         st.sync()
         assert np.max(np.abs(t.cpu().numpy() - exp)) < 1e-12
 
@@ -290,6 +295,9 @@ def test_qft30_c128_sampled_closed_form(fuse):
     t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
     st = qjp.State(t, basis=x)
     st.apply_circuit(C.qft(n).gates, fuse=fuse)
+    p = st.probabilities([0, 1, 2, 3])
+    assert abs(float(p.sum()) - 1) < 1e-10
+    st.canonicalize()
     st.sync()
     rng = np.random.default_rng(30)
     idx = np.unique(np.concatenate([rng.integers(0, 2**n, 1 << 16), [0, 1, 2**n - 1]])).astype(np.int64)
