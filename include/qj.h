@@ -214,6 +214,40 @@ const char* qj_last_error(void);
 /* Library version string. */
 const char* qj_version(void);
 
+/* ---- host-side planning (no GPU needed; exported for CPU tests) -------------
+ * qj_plan_circuit runs the same planner qj_apply_circuit uses on a state of
+ * n qubits split in `nshards` shards (a power of two; global qubits = top
+ * log2(nshards) bits) and returns its steps: per-shard passes on physical
+ * local bit positions, and EXCHANGE steps (global bit `gbit` <-> local bit
+ * `lbit`).  Gate data are read as complex128.  `phys` (n ints, may be NULL)
+ * receives the final logical->physical bit map.  Fused (TILE) steps are
+ * reported with type 2 and no payload.  Errors: INVALID_ARG / INDEX / OVERLAP
+ * as qj_apply_circuit, CAPACITY if more than max_steps steps, UNSUPPORTED for
+ * dense payloads larger than 4 targets. */
+typedef struct {
+    int type;                   /* 0 = pass, 1 = exchange, 2 = fused tile pass   */
+    int shard;                  /* global shard index the pass runs on            */
+    int kind;                   /* 0 dense, 1 x, 2 swap, 3 diag, 4 phase, 5 neg    */
+    int k;                      /* number of targets                              */
+    int tpos[QJ_MAX_TARGETS];   /* target bit positions, matrix order (MSB first) */
+    int nfix;                   /* fixed bits: controls / phase pattern           */
+    int fpos[64];
+    int fval[64];
+    uint32_t touch;             /* dense: touched-member mask (listed order)      */
+    int nm;                     /* complex values in m                            */
+    double m[2 * 256];          /* dense 4^k / diag 2^k / phase 1 (interleaved)   */
+    int gbit, lbit;             /* exchange                                       */
+    double alg_bytes;
+} qj_plan_step;
+
+qj_status qj_plan_circuit(int n, int nshards, int amp_bytes, const qj_gate* gates, int ngates,
+                          uint32_t flags, qj_plan_step* out, int max_steps, int* nsteps, int* phys);
+
+/* The exchange rule of the multi-GPU layer: for a swap of global bit `gbit`,
+ * rank `rank` trades with `*peer` the amplitudes of its shard whose swapped
+ * local bit equals `*half_bit`. */
+void qj_exchange_peer(int rank, int gbit, int* peer, int* half_bit);
+
 /* Host-side index math used by every pass (exported for exhaustive CPU
  * tests): insert a 0 bit at each of the `npos` ascending bit positions
  * `sorted_pos` into g (PAPER.md:221-227 listing, i1 = ((g>>m)<<(m+1)) + (g & (k-1))). */

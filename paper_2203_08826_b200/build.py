@@ -22,8 +22,19 @@ OBJ = os.path.join(ROOT, "build", "qj")
 LIB = os.path.join(PKG, "lib", "libqj.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_include():
+    """NCCL headers of the torch-bundled NCCL (the library is dlopen'ed at run time)."""
+    try:
+        import nvidia.nccl
+        return os.path.join(list(nvidia.nccl.__path__)[0], "include")
+    except Exception:
+        return "/usr/include"
+
+
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()]
 
 
 def _sources():

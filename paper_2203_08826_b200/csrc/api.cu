@@ -16,6 +16,7 @@
 #include "qj_internal.h"
 #include "planner.h"
 #include "common.cuh"
+#include "dist.h"
 
 using namespace qj;
 
@@ -52,6 +53,12 @@ struct qj_state_s {
     qj_counters ctr{};
     Planner planner;
     TileStaging stg;  // tile-pass program buffers
+    // multi-GPU (NCCL): one shard per process, global shard index = rank
+    void* comm = nullptr;  // ncclComm_t, nullptr for single-process states
+    int rank = 0, nranks = 1;
+    void* xbuf = nullptr;  // exchange staging ring
+    size_t xbuf_bytes = 0;
+    int total_shards() const { return comm ? nranks : (int)shards.size(); }
     // profiling: event pairs around passes
     bool profiling = false;
     struct Rec {
@@ -208,6 +215,70 @@ struct ProfScope {
 };
 
 // Execute planned steps on the device.
+// Exchange over NCCL (dist.h): this rank trades the half of its shard whose
+// local bit L equals spec.half_bit with the partner, chunk by chunk through
+// the staging ring.
+qj_status nccl_exchange(qj_state s, int j, int L) {
+    const char* why = nullptr;
+    const NcclApi* api = nccl_api(&why);
+    if (!api) return fail(QJ_ERR_NCCL, "NCCL unavailable: %s", why ? why : "?");
+    const ExchangeSpec ex = exchange_spec(s->rank, j);
+    const uint64_t half = 1ull << (s->nl - 1);
+    const uint64_t chunk = std::min<uint64_t>(half, (uint64_t)(256ull << 20) / (uint64_t)s->amp_bytes);
+    const bool contiguous = (L == s->nl - 1);
+    const size_t cb = (size_t)chunk * s->amp_bytes;
+    const size_t need = contiguous ? 2 * cb : 4 * cb;  // 2 receive slots (+ 2 pack slots)
+    if (s->xbuf_bytes < need) {
+        if (s->xbuf) {
+            cudaStreamSynchronize(s->stream);
+            cudaFree(s->xbuf);
+            s->xbuf = nullptr;
+            s->xbuf_bytes = 0;
+        }
+        cudaError_t e = cudaMalloc(&s->xbuf, need);
+        if (e != cudaSuccess) return cuda_fail(e, "exchange staging alloc");
+        s->xbuf_bytes = need;
+    }
+    unsigned char* state = static_cast<unsigned char*>(s->shards[0]);
+    unsigned char* stage = static_cast<unsigned char*>(s->xbuf);
+    ncclComm_t comm = static_cast<ncclComm_t>(s->comm);
+    const uint64_t base = (uint64_t)ex.half_bit << (s->nl - 1);  // contiguous case
+    cudaError_t e;
+    for (uint64_t h0 = 0, c = 0; h0 < half; h0 += chunk, ++c) {
+        const uint64_t cnt = std::min<uint64_t>(chunk, half - h0);
+        const size_t bytes = (size_t)cnt * s->amp_bytes;
+        unsigned char* recv = stage + (c & 1) * cb;
+        const unsigned char* send;
+        if (contiguous) {
+            send = state + (size_t)(base + h0) * s->amp_bytes;
+        } else {
+            unsigned char* pk = stage + (2 + (c & 1)) * cb;
+            e = launch_half_pack(state, pk, s->amp_bytes, L, ex.half_bit, h0, cnt, s->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "exchange pack");
+            s->ls.launches++;
+            send = pk;
+        }
+        ncclResult_t r = api->GroupStart();
+        if (r == ncclSuccess) r = api->Send(send, bytes, ncclInt8, ex.peer, comm, s->stream);
+        if (r == ncclSuccess) r = api->Recv(recv, bytes, ncclInt8, ex.peer, comm, s->stream);
+        const ncclResult_t r2 = api->GroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(QJ_ERR_NCCL, "exchange send/recv with rank %d: %s", ex.peer,
+                        api->GetErrorString(r != ncclSuccess ? r : r2));
+        if (contiguous) e = launch_copy(state + (size_t)(base + h0) * s->amp_bytes, recv, bytes, s->stream);
+        else e = launch_half_unpack(state, recv, s->amp_bytes, L, ex.half_bit, h0, cnt, s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "exchange unpack");
+        s->ls.launches++;
+    }
+    return QJ_OK;
+}
+
+// Device pointer of global shard `g` if this process owns it, else nullptr.
+void* shard_ptr(qj_state s, int g) {
+    if (s->comm) return g == s->rank ? s->shards[0] : nullptr;
+    return s->shards[(size_t)g];
+}
+
 qj_status execute(qj_state s, const std::vector<Step>& steps) {
     cudaError_t e = cudaSuccess;
     for (const Step& st : steps) {
@@ -216,6 +287,12 @@ qj_status execute(qj_state s, const std::vector<Step>& steps) {
             ProfScope prof(s, PROF_EXCHANGE, xb);
             // swap global bit (nl + j) with local bit L: pair shards r (bit j = 0) and r | 1<<j
             const int j = st.gbit, L = st.lbit;
+            if (s->comm) {
+                if (qj_status q = nccl_exchange(s, j, L)) return q;
+                s->ctr.exchanges++;
+                s->ctr.exchange_bytes += xb;
+                continue;
+            }
             for (size_t r = 0; r < s->shards.size(); ++r) {
                 if ((r >> j) & 1) continue;
                 const size_t r2 = r | (1ull << j);
@@ -233,12 +310,13 @@ qj_status execute(qj_state s, const std::vector<Step>& steps) {
             const size_t need = (size_t)s->amp_bytes * ((size_t)1 << (2 * st.pass.k));
             if (qj_status q = ensure_scratch(s, need)) return q;
         }
+        void* ptr = shard_ptr(s, st.shard);
+        if (!ptr) continue;  // another rank's shard
         ProfScope prof(s, st.type == Step::TILE ? PROF_TILE : st.pass.kind, st.alg_bytes);
         e = by_dtype(s->dt, [&](auto z) {
             using R = decltype(z);
-            if (st.type == Step::TILE)
-                return run_tile<R>(st.tile, s->shards[st.shard], s->nl, s->stream, s->stg, s->ls);
-            return run_pass<R>(st.pass, s->shards[st.shard], s->nl, s->stream, s->scratch, s->scratch_bytes, s->ls);
+            if (st.type == Step::TILE) return run_tile<R>(st.tile, ptr, s->nl, s->stream, s->stg, s->ls);
+            return run_pass<R>(st.pass, ptr, s->nl, s->stream, s->scratch, s->scratch_bytes, s->ls);
         });
         if (e != cudaSuccess) return cuda_fail(e, "pass launch");
         s->ctr.passes++;
@@ -250,7 +328,7 @@ qj_status execute(qj_state s, const std::vector<Step>& steps) {
 
 qj_status apply_lgates(qj_state s, const std::vector<LGate>& gates, bool fuse) {
     std::vector<Step> steps;
-    PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, (int)s->shards.size(), &s->phys};
+    PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, s->total_shards(), &s->phys};
     s->planner.plan(ctx, gates, fuse, steps);
     return execute(s, steps);
 }
@@ -270,15 +348,18 @@ uint64_t qj_insert_zero_bits(uint64_t g, const int* sorted_pos, int npos) {
 }
 
 static qj_status init_common(qj_state* out, void* const* shards, int nshards, int n, qj_dtype dt,
-                             uint64_t basis_index, void* cuda_stream) {
+                             uint64_t basis_index, void* cuda_stream, void* comm = nullptr, int rank = 0,
+                             int nranks = 1) {
     if (!out) return fail(QJ_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (!dtype_ok(dt)) return fail(QJ_ERR_DTYPE, "unknown dtype %d", (int)dt);
     if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
     if (nshards < 1 || (nshards & (nshards - 1))) return fail(QJ_ERR_INVALID_ARG, "nshards=%d is not a power of two", nshards);
+    if (nranks < 1 || (nranks & (nranks - 1))) return fail(QJ_ERR_INVALID_ARG, "%d ranks is not a power of two", nranks);
+    const int ptot = comm ? nranks : nshards;
     int g = 0;
-    while ((1 << g) < nshards) ++g;
-    if (g >= n) return fail(QJ_ERR_CAPACITY, "%d shards need more than n=%d qubits", nshards, n);
+    while ((1 << g) < ptot) ++g;
+    if (g >= n) return fail(QJ_ERR_CAPACITY, "%d shards need more than n=%d qubits", ptot, n);
     if (!shards) return fail(QJ_ERR_INVALID_ARG, "amplitude buffer is NULL");
     for (int r = 0; r < nshards; ++r) {
         if (!shards[r]) return fail(QJ_ERR_INVALID_ARG, "shard %d buffer is NULL", r);
@@ -296,6 +377,9 @@ static qj_status init_common(qj_state* out, void* const* shards, int nshards, in
     s->amp_bytes = dt == QJ_C64 ? 8 : 16;
     s->shards.assign(shards, shards + nshards);
     s->stream = static_cast<cudaStream_t>(cuda_stream);
+    s->comm = comm;
+    s->rank = rank;
+    s->nranks = nranks;
     s->phys.resize(n);
     for (int q = 0; q < n; ++q) s->phys[q] = n - 1 - q;  // reading R1
     *out = s;
@@ -312,10 +396,16 @@ static qj_status init_common(qj_state* out, void* const* shards, int nshards, in
 
 qj_status qj_state_init(qj_state* out, void* amps_dev, int n, qj_dtype dt, uint64_t basis_index, void* cuda_stream,
                         void* nccl_comm) {
-    if (nccl_comm != nullptr)
-        return fail(QJ_ERR_UNSUPPORTED, "NCCL-sharded states are created with qj_state_init_nccl");
     void* shards[1] = {amps_dev};
-    return init_common(out, shards, 1, n, dt, basis_index, cuda_stream);
+    if (nccl_comm == nullptr) return init_common(out, shards, 1, n, dt, basis_index, cuda_stream);
+    const char* why = nullptr;
+    const NcclApi* api = nccl_api(&why);
+    if (!api) return fail(QJ_ERR_NCCL, "NCCL unavailable: %s", why ? why : "?");
+    int rank = 0, count = 1;
+    ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+    if (api->CommUserRank(comm, &rank) != ncclSuccess || api->CommCount(comm, &count) != ncclSuccess)
+        return fail(QJ_ERR_NCCL, "could not query the NCCL communicator");
+    return init_common(out, shards, 1, n, dt, basis_index, cuda_stream, nccl_comm, rank, count);
 }
 
 qj_status qj_state_init_sharded(qj_state* out, void* const* shards, int nshards, int n, qj_dtype dt,
@@ -331,10 +421,11 @@ qj_status qj_state_reset(qj_state s, uint64_t basis_index) {
     for (int q = 0; q < s->n; ++q) s->phys[q] = s->n - 1 - q;
     const uint64_t owner = basis_index >> s->nl;
     const uint64_t local = basis_index & ((1ull << s->nl) - 1);
-    for (size_t r = 0; r < s->shards.size(); ++r) {
+    for (size_t i = 0; i < s->shards.size(); ++i) {
+        const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
         cudaError_t e = by_dtype(s->dt, [&](auto z) {
             using R = decltype(z);
-            return run_init<R>(s->shards[r], s->nl, local, r == owner, s->stream, s->ls);
+            return run_init<R>(s->shards[i], s->nl, local, r == owner, s->stream, s->ls);
         });
         if (e != cudaSuccess) return cuda_fail(e, "init launch");
     }
@@ -393,6 +484,7 @@ qj_status qj_state_free(qj_state s) {
     s->stg.release();
     if (s->scratch) cudaFree(s->scratch);
     if (s->bins) cudaFree(s->bins);
+    if (s->xbuf) cudaFree(s->xbuf);
     delete s;
     return QJ_OK;
 }
@@ -402,7 +494,7 @@ qj_status qj_state_info(qj_state s, int* n, int* n_local, int* dtype, int* nshar
     if (n) *n = s->n;
     if (n_local) *n_local = s->nl;
     if (dtype) *dtype = (int)s->dt;
-    if (nshards) *nshards = (int)s->shards.size();
+    if (nshards) *nshards = s->total_shards();
     return QJ_OK;
 }
 
@@ -490,19 +582,23 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
         bool identity = true;
         for (int q = 0; q < n; ++q) identity &= (s->phys[q] == n - 1 - q);
         const size_t rb = s->dt == QJ_C64 ? 4 : 8;
-        for (size_t r = 0; r < s->shards.size(); ++r) {
+        if (s->comm && !identity)
+            return fail(QJ_ERR_UNSUPPORTED, "full probabilities of a remapped NCCL-sharded state: call qj_state_canonicalize first");
+        for (size_t i = 0; i < s->shards.size(); ++i) {
+            const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
             if (identity) {
-                void* dst = static_cast<unsigned char*>(out_dev) + rb * (r << nl);
+                // NCCL-sharded: out_dev holds this rank's 2^n_local values
+                void* dst = static_cast<unsigned char*>(out_dev) + (s->comm ? 0 : rb * (r << nl));
                 e = by_dtype(s->dt, [&](auto z) {
                     using R = decltype(z);
-                    return run_prob_full<R>(s->shards[r], nl, dst, s->stream, s->ls);
+                    return run_prob_full<R>(s->shards[i], nl, dst, s->stream, s->ls);
                 });
             } else {
                 int cpos[64];
                 for (int q = 0; q < n; ++q) cpos[s->phys[q]] = n - 1 - q;
                 e = by_dtype(s->dt, [&](auto z) {
                     using R = decltype(z);
-                    return run_prob_scatter<R>(s->shards[r], nl, r, n, cpos, out_dev, s->stream, s->ls);
+                    return run_prob_scatter<R>(s->shards[i], nl, r, n, cpos, out_dev, s->stream, s->ls);
                 });
             }
             if (e != cudaSuccess) return cuda_fail(e, "probabilities launch");
@@ -524,7 +620,8 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
     if (qj_status st = ensure_bins(s, nb)) return st;
     e = cudaMemsetAsync(s->bins, 0, nb * sizeof(double), s->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bins memset");
-    for (size_t r = 0; r < s->shards.size(); ++r) {
+    for (size_t i = 0; i < s->shards.size(); ++i) {
+        const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
         int pos[64], gv[64];
         for (int i = 0; i < nq; ++i) {
             const int b = s->phys[qubits[i]];
@@ -538,9 +635,17 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
         }
         e = by_dtype(s->dt, [&](auto z) {
             using R = decltype(z);
-            return run_prob_marginal<R>(s->shards[r], nl, pos, gv, nq, s->bins, s->stream, s->ls);
+            return run_prob_marginal<R>(s->shards[i], nl, pos, gv, nq, s->bins, s->stream, s->ls);
         });
         if (e != cudaSuccess) return cuda_fail(e, "marginal launch");
+    }
+    if (s->comm) {  // sum the per-rank fp64 bins across ranks
+        const char* why = nullptr;
+        const NcclApi* api = nccl_api(&why);
+        if (!api) return fail(QJ_ERR_NCCL, "NCCL unavailable: %s", why ? why : "?");
+        const ncclResult_t r = api->AllReduce(s->bins, s->bins, nb, ncclFloat64, ncclSum,
+                                              static_cast<ncclComm_t>(s->comm), s->stream);
+        if (r != ncclSuccess) return fail(QJ_ERR_NCCL, "marginal all-reduce: %s", api->GetErrorString(r));
     }
     e = by_dtype(s->dt, [&](auto z) {
         using R = decltype(z);
@@ -548,6 +653,73 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
     });
     if (e != cudaSuccess) return cuda_fail(e, "bins launch");
     s->ctr.launches = s->ls.launches;
+    return QJ_OK;
+}
+
+void qj_exchange_peer(int rank, int gbit, int* peer, int* half_bit) {
+    const ExchangeSpec e = exchange_spec(rank, gbit);
+    if (peer) *peer = e.peer;
+    if (half_bit) *half_bit = e.half_bit;
+}
+
+qj_status qj_plan_circuit(int n, int nshards, int amp_bytes, const qj_gate* gates, int ngates, uint32_t flags,
+                          qj_plan_step* out, int max_steps, int* nsteps, int* phys) {
+    if (!nsteps || (max_steps > 0 && !out)) return fail(QJ_ERR_INVALID_ARG, "NULL output");
+    if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
+    if (nshards < 1 || (nshards & (nshards - 1))) return fail(QJ_ERR_INVALID_ARG, "nshards=%d is not a power of two", nshards);
+    if (ngates < 0 || (ngates > 0 && !gates)) return fail(QJ_ERR_INVALID_ARG, "bad gate list");
+    if (flags & ~QJ_FUSE) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    qj_state_s tmp;  // host-only view: n, dtype complex128
+    tmp.n = n;
+    tmp.dt = QJ_C128;
+    int g = 0;
+    while ((1 << g) < nshards) ++g;
+    if (g >= n) return fail(QJ_ERR_CAPACITY, "%d shards need more than n=%d qubits", nshards, n);
+    std::vector<LGate> gs((size_t)ngates);
+    for (int i = 0; i < ngates; ++i) {
+        const qj_gate& q = gates[i];
+        if (q.nt > QJ_MAX_TARGETS || q.nc > QJ_MAX_CONTROLS)
+            return fail(QJ_ERR_TOO_MANY_TARGETS, "gate %d: nt=%d nc=%d exceeds the limits", i, q.nt, q.nc);
+        qj_status st = make_lgate(&tmp, q.kind, q.targets, q.nt, q.controls, q.nc, q.data, gs[(size_t)i]);
+        if (st != QJ_OK) return st;
+    }
+    std::vector<int> map(n);
+    for (int q = 0; q < n; ++q) map[q] = n - 1 - q;
+    PlanContext ctx{n, n - g, g, amp_bytes, nshards, &map};
+    std::vector<Step> steps;
+    Planner pl;
+    pl.plan(ctx, gs, (flags & QJ_FUSE) != 0, steps);
+    if ((int)steps.size() > max_steps) return fail(QJ_ERR_CAPACITY, "plan has %zu steps > %d", steps.size(), max_steps);
+    for (size_t i = 0; i < steps.size(); ++i) {
+        const Step& st = steps[i];
+        qj_plan_step& o = out[i];
+        std::memset(&o, 0, sizeof(o));
+        o.type = (int)st.type;
+        o.shard = st.shard;
+        o.gbit = st.gbit;
+        o.lbit = st.lbit;
+        o.alg_bytes = st.alg_bytes;
+        if (st.type != Step::PASS) continue;
+        const Pass& p = st.pass;
+        o.kind = p.kind;
+        o.k = p.k;
+        for (int j = 0; j < p.k; ++j) o.tpos[j] = p.tpos[j];
+        o.nfix = p.nfix;
+        for (int j = 0; j < p.nfix; ++j) {
+            o.fpos[j] = p.fpos[j];
+            o.fval[j] = p.fval[j];
+        }
+        o.touch = p.touch;
+        if (p.m.size() > 256) return fail(QJ_ERR_UNSUPPORTED, "plan export: payload of %zu values", p.m.size());
+        o.nm = (int)p.m.size();
+        for (size_t j = 0; j < p.m.size(); ++j) {
+            o.m[2 * j] = p.m[j].real();
+            o.m[2 * j + 1] = p.m[j].imag();
+        }
+    }
+    *nsteps = (int)steps.size();
+    if (phys)
+        for (int q = 0; q < n; ++q) phys[q] = map[q];
     return QJ_OK;
 }
 

@@ -29,7 +29,8 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_apply_gate", "qj_apply_x", "qj_apply_z", "qj_apply_swap", "qj_apply_fsim",
            "qj_apply_diagonal", "qj_apply_circuit", "qj_probabilities", "qj_sync",
            "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
-           "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize"]
+           "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
+           "qj_plan_circuit", "qj_exchange_peer"]
 
 
 class QJError(RuntimeError):
@@ -54,6 +55,14 @@ class qj_counters(ctypes.Structure):
 class qj_profile_entry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64),
                 ("total_ms", ctypes.c_double), ("alg_bytes", ctypes.c_double)]
+
+
+class qj_plan_step(ctypes.Structure):
+    _fields_ = [("type", ctypes.c_int), ("shard", ctypes.c_int), ("kind", ctypes.c_int), ("k", ctypes.c_int),
+                ("tpos", ctypes.c_int * MAX_TARGETS), ("nfix", ctypes.c_int), ("fpos", ctypes.c_int * 64),
+                ("fval", ctypes.c_int * 64), ("touch", ctypes.c_uint32), ("nm", ctypes.c_int),
+                ("m", ctypes.c_double * 512), ("gbit", ctypes.c_int), ("lbit", ctypes.c_int),
+                ("alg_bytes", ctypes.c_double)]
 
 
 _lib = None
@@ -91,6 +100,9 @@ def lib():
         "qj_set_profiling": ([P, I], S),
         "qj_get_profile": ([P, ctypes.POINTER(qj_profile_entry), I, IP, I], S),
         "qj_state_canonicalize": ([P], S),
+        "qj_plan_circuit": ([I, I, I, ctypes.POINTER(qj_gate), I, ctypes.c_uint32, ctypes.POINTER(qj_plan_step), I,
+                             IP, IP], S),
+        "qj_exchange_peer": ([I, I, IP, IP], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -113,6 +125,65 @@ def _ints(xs):
 def insert_zero_bits(g: int, sorted_positions) -> int:
     arr, n = _ints(sorted_positions)
     return int(lib().qj_insert_zero_bits(ctypes.c_uint64(g), arr, n))
+
+
+def exchange_peer(rank: int, gbit: int):
+    """(peer rank, value of the swapped local bit of the half this rank trades)."""
+    p, h = ctypes.c_int(), ctypes.c_int()
+    lib().qj_exchange_peer(int(rank), int(gbit), ctypes.byref(p), ctypes.byref(h))
+    return p.value, h.value
+
+
+def pack_gates(gates, np_dtype=np.complex128):
+    """Marshal gate records (kind/targets/controls/data) into a qj_gate array."""
+    gates = list(gates)
+    arr = (qj_gate * max(1, len(gates)))()
+    keep = []
+    for i, g in enumerate(gates):
+        e = arr[i]
+        e.kind = KIND[g.kind]
+        e.nt = len(g.targets)
+        e.nc = len(g.controls)
+        if e.nt > MAX_TARGETS or e.nc > MAX_CONTROLS:
+            raise QJError(4, f"gate {i}: too many qubits")
+        for j, q in enumerate(g.targets):
+            e.targets[j] = int(q)
+        for j, q in enumerate(g.controls):
+            e.controls[j] = int(q)
+        if g.kind == "dense":
+            d = np.asarray(g.data[0], dtype=np_dtype).reshape(-1)
+        elif g.kind == "diag":
+            d = np.asarray(g.data[0], dtype=np_dtype).reshape(-1)
+        elif g.kind == "fsim":
+            d = np.asarray(list(np.asarray(g.data[0]).reshape(-1)) + [g.data[1]], dtype=np_dtype)
+        else:
+            d = None
+        if d is not None:
+            d = np.ascontiguousarray(d)
+            keep.append(d)
+            e.data = d.ctypes.data
+        else:
+            e.data = None
+    return arr, len(gates), keep
+
+
+def plan_circuit(n, nshards, gates, fuse=False, amp_bytes=16, max_steps=1 << 16):
+    """Run the library's host planner (no GPU): returns (steps, phys map)."""
+    arr, ng, keep = pack_gates(gates)
+    out = (qj_plan_step * max_steps)()
+    cnt = ctypes.c_int()
+    phys = (ctypes.c_int * n)()
+    _check(lib().qj_plan_circuit(n, nshards, amp_bytes, arr, ng, QJ_FUSE if fuse else 0, out, max_steps,
+                                 ctypes.byref(cnt), phys))
+    del keep
+    steps = []
+    for i in range(cnt.value):
+        o = out[i]
+        m = np.array(o.m[:2 * o.nm]).view(np.complex128) if o.nm else np.zeros(0, np.complex128)
+        steps.append({"type": o.type, "shard": o.shard, "kind": o.kind, "tpos": list(o.tpos[:o.k]),
+                      "fix": [(o.fpos[j], o.fval[j]) for j in range(o.nfix)], "touch": o.touch, "m": m,
+                      "gbit": o.gbit, "lbit": o.lbit, "alg_bytes": o.alg_bytes})
+    return steps, list(phys)
 
 
 class State:
@@ -157,6 +228,33 @@ class State:
     @classmethod
     def sharded(cls, shards, n, basis=0, stream=None):
         return cls(None, basis=basis, stream=stream, _shards=list(shards), _n=n)
+
+    @classmethod
+    def distributed(cls, tensor, n, group=None, basis=0, stream=None):
+        """One shard per process: `tensor` holds this rank's 2^(n - log2 P)
+        amplitudes (global qubits = the top log2 P bits, shard index = rank).
+        The NCCL communicator is torch's (ProcessGroupNCCL); it is initialised
+        eagerly with a barrier before its pointer is taken."""
+        import torch
+        import torch.distributed as dist
+
+        pg = group if group is not None else dist.group.WORLD
+        dist.barrier(group=pg, device_ids=[tensor.device.index])
+        comm = pg._get_backend(torch.device("cuda"))._comm_ptr()
+        self = cls.__new__(cls)
+        L = lib()
+        self._h = ctypes.c_void_p()
+        self.dtype = QJ_C64 if tensor.dtype == torch.complex64 else QJ_C128
+        self.np_dtype = np.complex64 if self.dtype == QJ_C64 else np.complex128
+        self.real_dtype = torch.float32 if self.dtype == QJ_C64 else torch.float64
+        self.n = n
+        self.shards = [tensor]
+        self.device = tensor.device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(L.qj_state_init(ctypes.byref(self._h), ctypes.c_void_p(tensor.data_ptr()), n, self.dtype,
+                               ctypes.c_uint64(QJ_KEEP if basis is None else int(basis)),
+                               ctypes.c_void_p(self.stream.cuda_stream), ctypes.c_void_p(comm)))
+        return self
 
     # -- lifetime ----------------------------------------------------------
     def free(self):
@@ -221,35 +319,8 @@ class State:
 
     def pack_circuit(self, gates):
         """Marshal gate records (objects with kind/targets/controls/data, e.g.
-        workloads.gates.Gate) into a qj_gate array; returns (array, keepalive)."""
-        gates = list(gates)
-        arr = (qj_gate * max(1, len(gates)))()
-        keep = []
-        for i, g in enumerate(gates):
-            e = arr[i]
-            e.kind = KIND[g.kind]
-            e.nt = len(g.targets)
-            e.nc = len(g.controls)
-            if e.nt > MAX_TARGETS or e.nc > MAX_CONTROLS:
-                raise QJError(4, f"gate {i}: too many qubits")
-            for j, q in enumerate(g.targets):
-                e.targets[j] = int(q)
-            for j, q in enumerate(g.controls):
-                e.controls[j] = int(q)
-            if g.kind == "dense":
-                d = self._mat(g.data[0], 4 ** e.nt)
-            elif g.kind == "diag":
-                d = self._mat(g.data[0], 2 ** e.nt)
-            elif g.kind == "fsim":
-                d = self._mat(list(np.asarray(g.data[0]).reshape(-1)) + [g.data[1]], 5)
-            else:
-                d = None
-            if d is not None:
-                keep.append(d)
-                e.data = d.ctypes.data
-            else:
-                e.data = None
-        return arr, len(gates), keep
+        workloads.gates.Gate) into a qj_gate array; returns (array, n, keepalive)."""
+        return pack_gates(gates, self.np_dtype)
 
     def apply_circuit(self, gates, fuse=False, packed=None):
         arr, ng, keep = packed if packed is not None else self.pack_circuit(gates)

@@ -309,3 +309,44 @@ def test_qft30_c128_sampled_closed_form(fuse):
     assert abs(float(p.sum()) - 1) < 1e-10
     del st, t
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------ NCCL path (1 rank on 1 GPU)
+def _nccl_worker(port, q):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    try:
+        n = 12
+        circ = C.qft(n)
+        t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+        st = qjp.State.distributed(t, n, basis=5)
+        st.apply_circuit(circ.gates)
+        p = st.probabilities([0, 3, 7]).cpu().numpy()    # NCCL all-reduce of the bins
+        full = st.probabilities().cpu().numpy()
+        st.sync()
+        exp = oracle.run(circ, oracle.basis_state(n, 5))
+        q.put((float(np.max(np.abs(t.cpu().numpy() - exp))),
+               float(np.max(np.abs(p - oracle.probabilities(exp, n, [0, 3, 7])))),
+               float(np.max(np.abs(full - np.abs(exp) ** 2))), st.info()["nshards"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_single_rank_state():
+    import multiprocessing as mpm
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mpm.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(port, q))
+    p.start()
+    p.join(timeout=300)
+    assert p.exitcode == 0
+    e_amp, e_marg, e_full, nsh = q.get(timeout=10)
+    assert nsh == 1 and e_amp < 1e-12 and e_marg < 1e-12 and e_full < 1e-12
