@@ -16,9 +16,16 @@ Arms:
                    host cores: each step applies a bounded sample of the QFT30
                    gates to a 2^30 state and extrapolates to s/circuit.
 
+By default the fused planner runs (window tile passes, one HBM round trip per
+run of gates); the per-gate-pass numbers (`--no-fuse` path) are measured in the
+same run and reported under "unfused".
+
 Multi-GPU (torchrun, N>1): every rank runs its own QFT30 circuit (independent
 problems, weak scaling, no data-path collective); the max over ranks of the
-device time is used and value = that time / (steps * N).
+device time is used and value = that time / (steps * N).  The same run then
+times QFT(30 + log2 N) sharded over the N ranks through NCCL global-qubit
+swaps and reports it under "sharded" (a watchdog keeps a hang from losing the
+line).
 """
 
 from __future__ import annotations
@@ -182,6 +189,136 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------- qj arm
+def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True):
+    """Time `steps` steps (state reset + circuit + 10-qubit marginal) on the
+    device with CUDA events; returns timings, per-kind profile and counters."""
+    n = wl["n"]
+    tdt = torch.complex128 if wl["dtype"] == "c128" else torch.complex64
+    stream = torch.cuda.Stream(dev)
+    psi = torch.empty(1 << n, dtype=tdt, device=dev)
+    st = qj.State(psi, basis=None, stream=stream)
+    packed = st.pack_circuit(wl["circ"].gates)
+    readout = wl["readout"]
+    pbuf = torch.empty(1 << len(readout), dtype=st.real_dtype, device=dev)
+
+    def step():
+        st.reset(wl["basis"])
+        st.apply_circuit(None, fuse=fuse, packed=packed)
+        st.probabilities(readout, out=pbuf)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    step()  # dry run (P:400-404): first circuit of this configuration
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dry = ev0.elapsed_time(ev1) / 1e3
+    for _ in range(max(0, warmup - 1)):
+        step()
+    barrier()
+    st.counters(reset=True)
+    if profile:
+        st.set_profiling(True)
+        st.profile(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    prof = st.profile(reset=True) if profile else {}
+    st.set_profiling(False)
+    ctr = st.counters(reset=True)
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+    return dict(st=st, psi=psi, stream=stream, pbuf=pbuf, ms=ms, ms_max=ms_max, prof=prof, ctr=ctr,
+                clk=clk, dry=dry)
+
+
+def roofline_of(prof, ms_step_total, peak, peak_src, traffic, traffic_src):
+    if not prof:
+        return None
+    k, d = max(prof.items(), key=lambda kv: kv[1]["total_ms"])
+    ach = d["alg_bytes"] / (d["total_ms"] / 1e3) / 1e9
+    tr = traffic.get(k) if traffic else None
+    return {"bound": "hbm", "kernel": k, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": peak_src, "alg_bytes_per_launch": d["alg_bytes"] / d["launches"],
+            "avg_launch_us": d["total_ms"] / d["launches"] * 1e3,
+            "share_of_step": d["total_ms"] / max(ms_step_total, 1e-9),
+            "traffic": (tr["dram_bytes_per_launch"] if tr else None), "traffic_source": traffic_src}
+
+
+def kinds_of(prof, steps, peak):
+    return {k: {"launches_per_step": v["launches"] / steps, "ms_per_step": v["total_ms"] / steps,
+                "GBps": v["alg_bytes"] / max(v["total_ms"], 1e-12) / 1e6,
+                "frac": v["alg_bytes"] / max(v["total_ms"], 1e-12) / 1e6 / peak} for k, v in prof.items()}
+
+
+def sharded_section(qj, torch, dev, world, rank, timeout_s, emit):
+    """QFT(30 + log2 N) complex128 sharded over the N ranks (16 GiB per GPU):
+    global-qubit swaps run as NCCL exchanges.  One warm-up and one timed
+    circuit; a watchdog keeps a hang from losing the main line."""
+    import threading
+    from workloads import circuits as C
+
+    g = world.bit_length() - 1
+    n = 30 + g
+
+    def on_timeout():
+        emit({"error": f"timeout after {timeout_s}s"})
+        os._exit(0)
+
+    wd = threading.Timer(timeout_s, on_timeout)
+    wd.daemon = True
+    wd.start()
+    try:
+        t = torch.empty(1 << (n - g), dtype=torch.complex128, device=dev)
+        stream = torch.cuda.Stream(dev)
+        with torch.cuda.stream(stream):
+            st = qj.State.distributed(t, n, basis=SEED_X, stream=stream)
+        circ = C.qft(n)
+        packed = st.pack_circuit(circ.gates)
+        pb = torch.empty(1 << 10, dtype=torch.float64, device=dev)
+        st.apply_circuit(None, packed=packed)
+        st.sync()
+        st.reset(SEED_X)
+        torch.cuda.synchronize(dev)
+        torch.distributed.barrier()
+        st.counters(reset=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st.apply_circuit(None, packed=packed)
+        st.probabilities(list(range(10)), out=pb)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        ctr = st.counters(reset=True)
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        psum = float(pb.sum().item())
+        res = {"workload": f"qft{n}_c128_sharded", "n": n, "ranks": world, "s_per_circuit": float(tt.item()) / 1e3,
+               "exchanges": ctr["exchanges"], "exchange_bytes_per_rank": ctr["exchange_bytes"],
+               "alg_bytes_per_rank": ctr["alg_bytes"], "marginal_sum": psum,
+               "note": "per-gate passes + NCCL local<->global swaps (fused planning is single-shard only)"}
+        st.free()
+        return res
+    except Exception as e:  # report, never lose the main line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+    finally:
+        wd.cancel()
+
+
 def run_qj(args, rank, world):
     import numpy as np
     import torch
@@ -192,80 +329,38 @@ def run_qj(args, rank, world):
     torch.cuda.set_device(dev)
     wl = make_workload(args.workload)
     n = wl["n"]
-    tdt = torch.complex128 if wl["dtype"] == "c128" else torch.complex64
     amp_bytes = 16 if wl["dtype"] == "c128" else 8
     t_load0 = time.perf_counter()
     qj.lib()
-    stream = torch.cuda.Stream(dev)
-    psi = torch.empty(1 << n, dtype=tdt, device=dev)
-    st = qj.State(psi, basis=None, stream=stream)
-    gates = wl["circ"].gates
-    packed = st.pack_circuit(gates)
-    readout = wl["readout"]
-    pbuf = torch.empty(1 << len(readout), dtype=st.real_dtype, device=dev)
-
-    def step():
-        st.reset(wl["basis"])
-        st.apply_circuit(None, fuse=args.fuse, packed=packed)
-        st.probabilities(readout, out=pbuf)
-
-    def barrier():
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            torch.distributed.barrier()
-
-    # dry run: first circuit after library load
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        ev0.record(stream)
-        step()
-        ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    dry_run_s = ev0.elapsed_time(ev1) / 1e3
     load_s = time.perf_counter() - t_load0
-    for _ in range(max(0, args.warmup - 1)):
-        step()
-    barrier()
+    steps = args.steps
+    peak, peak_src = load_peaks()
+    traffic, traffic_src = load_traffic()
 
-    # ---- timed region (device events, per-pass profiling events on) ----
-    st.counters(reset=True)
-    st.set_profiling(True)
-    st.profile(reset=True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    with ClockSampler(dev.index) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-    barrier()
-    ms = e0.elapsed_time(e1)
-    prof = st.profile(reset=True)
-    st.set_profiling(False)
-    ctr = st.counters(reset=True)
-    ms_max = ms
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_max = float(t.item())
+    # ---- headline: the default planner (fused window passes unless --no-fuse)
+    m = measure(qj, torch, wl, args.fuse, steps, args.warmup, dev, world)
+    st, psi, stream = m["st"], m["psi"], m["stream"]
 
     # ---- e2e: the public API with host buffers each step ----
+    readout = wl["readout"]
     host_out = torch.empty(1 << len(readout), dtype=st.real_dtype, pin_memory=True)
     h2d = 0
+    gates = wl["circ"].gates
     for g in gates:
         h2d += 112  # sizeof(qj_gate)
         if g.kind in ("dense", "diag", "fsim"):
             cnt = {"dense": 4 ** len(g.targets), "diag": 2 ** len(g.targets), "fsim": 5}[g.kind]
             h2d += cnt * amp_bytes
     d2h = host_out.numel() * host_out.element_size()
-    barrier()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         st.reset(wl["basis"])
-        st.apply_circuit(gates, fuse=args.fuse)           # packs host gate list each step
-        p = st.probabilities(readout, out=pbuf)
+        st.apply_circuit(gates, fuse=args.fuse)           # packs the host gate list each step
+        p = st.probabilities(readout, out=m["pbuf"])
         with torch.cuda.stream(stream):
             host_out.copy_(p, non_blocking=True)
         stream.synchronize()
@@ -280,43 +375,41 @@ def run_qj(args, rank, world):
     # ---- parity spot check of the benched state (not timed) ----
     check = None
     if args.workload.startswith("qft"):
+        st.canonicalize()
         rng = np.random.default_rng(30)
         idx = np.unique(np.concatenate([rng.integers(0, 1 << n, 4096), [0, (1 << n) - 1]])).astype(np.int64)
         got = psi[torch.from_numpy(idx).to(dev)].cpu().numpy()
-        m = (np.uint64(wl["basis"]) * idx.astype(np.uint64)) % np.uint64(1 << n)
-        exp = 2 ** (-n / 2) * np.exp(2j * np.pi * m.astype(np.float64) / (1 << n))
+        mm = (np.uint64(wl["basis"]) * idx.astype(np.uint64)) % np.uint64(1 << n)
+        exp = 2 ** (-n / 2) * np.exp(2j * np.pi * mm.astype(np.float64) / (1 << n))
         check = float(np.max(np.abs(got - exp)))
+    st.free()
+    del psi, m["psi"]
+    torch.cuda.empty_cache()
 
-    if rank != 0:
-        return 0
-    steps = args.steps
+    # ---- per-gate passes (the north star's "per gate pass" bandwidth) ----
+    unfused = None
+    if args.fuse and not args.no_unfused:
+        u = measure(qj, torch, wl, False, max(1, min(steps, 3)), 1, dev, world)
+        us = max(1, min(steps, 3))
+        ub = u["ctr"]["alg_bytes"] / us
+        unfused = {"value": u["ms_max"] / 1e3 / (us * world), "unit": "s/circuit", "steps": us,
+                   "effective_gbs": ub / (u["ms_max"] / us / 1e3) / 1e9,
+                   "effective_frac": ub / (u["ms_max"] / us / 1e3) / 1e9 / peak,
+                   "roofline": roofline_of(u["prof"], u["ms"], peak, peak_src, traffic, traffic_src),
+                   "kinds": kinds_of(u["prof"], us, peak), "gpu_launches": u["ctr"]["launches"]}
+        u["st"].free()
+        del u
+        torch.cuda.empty_cache()
+
+    ms_max = m["ms_max"]
     value = ms_max / 1e3 / (steps * world)
-    per_step_bytes = ctr["alg_bytes"] / steps
-    peak, peak_src = load_peaks()
-    traffic, traffic_src = load_traffic()
-    dom = max(prof.items(), key=lambda kv: kv[1]["total_ms"]) if prof else (None, None)
-    roof = None
-    if dom[0]:
-        k, d = dom
-        ach = d["alg_bytes"] / (d["total_ms"] / 1e3) / 1e9
-        per_launch = d["alg_bytes"] / d["launches"]
-        tr = traffic.get(k) if traffic else None
-        roof = {"bound": "hbm", "kernel": k, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "peak_source": peak_src,
-                "alg_bytes_per_launch": per_launch,
-                "avg_launch_us": d["total_ms"] / d["launches"] * 1e3,
-                "share_of_step": d["total_ms"] / max(ms, 1e-9),
-                "traffic": (tr["dram_bytes_per_launch"] if tr else None),
-                "traffic_source": traffic_src}
-    kinds = {k: {"launches_per_step": v["launches"] / steps, "ms_per_step": v["total_ms"] / steps,
-                 "GBps": v["alg_bytes"] / max(v["total_ms"], 1e-12) / 1e6,
-                 "frac": v["alg_bytes"] / max(v["total_ms"], 1e-12) / 1e6 / peak}
-             for k, v in prof.items()}
+    per_step_bytes = m["ctr"]["alg_bytes"] / steps
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and rank == 0:
         v, sample, cores = oracle_sample(wl)
         cpu = {"value": v, "unit": "s/circuit", "cores": cores, "kind": "oracle",
                "sample": f"one gate per class on a 2^{n} state, extrapolated by class counts: {sample}"}
+    state_bytes = amp_bytes << n
     line = {
         "metric": METRIC, "value": value, "unit": "s/circuit", "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms_max / steps, "higher_is_better": False,
@@ -325,22 +418,34 @@ def run_qj(args, rank, world):
         "config": {"workload": args.workload, "n": n, "state": wl["dtype"], "gates": len(gates),
                    "basis": wl["basis"], "fuse": bool(args.fuse),
                    "step": "state_reset + apply_circuit + 10-qubit marginal probabilities",
-                   "l2": f"state {amp_bytes << n >> 20} MiB >> 126 MB L2: inputs larger than L2, no flush",
-                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU"},
+                   "l2": (f"state {state_bytes >> 20} MiB >> 126 MB L2: inputs larger than L2, no flush"
+                          if state_bytes > (256 << 20) else
+                          f"state {state_bytes >> 20} MiB is L2-resident (no flush; latency/L2-bound regime)"),
+                   "parallelism": f"{world} independent replicas (weak scaling)" if world > 1 else "1 GPU"},
         "effective_gbs": per_step_bytes / (ms_max / steps / 1e3) / 1e9,
         "effective_frac": per_step_bytes / (ms_max / steps / 1e3) / 1e9 / peak,
         "alg_bytes_per_step": per_step_bytes,
-        "roofline": roof,
-        "kinds": kinds,
+        "roofline": roofline_of(m["prof"], m["ms"], peak, peak_src, traffic, traffic_src),
+        "kinds": kinds_of(m["prof"], steps, peak),
+        "unfused": unfused,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_ms / 1e3 / (steps * world), "unit": "s/circuit",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": ctr["launches"],
-        "clocks": clk.summary(),
-        "dry_run_s": dry_run_s, "first_call_incl_load_s": load_s,
+        "gpu_launches": m["ctr"]["launches"],
+        "clocks": m["clk"].summary(),
+        "dry_run_s": m["dry"], "lib_load_s": load_s,
         "parity_max_abs_err_sampled": check,
     }
-    print(json.dumps(line), flush=True)
+
+    def emit(sharded):
+        if rank == 0:
+            line["sharded"] = sharded
+            print(json.dumps(line), flush=True)
+
+    if world > 1 and not args.no_sharded:
+        emit(sharded_section(qj, torch, dev, world, rank, args.sharded_timeout, emit))
+    else:
+        emit(None)
     return 0
 
 
@@ -351,9 +456,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="qj", choices=["qj", "reference"])
     ap.add_argument("--workload", default="qft30_c128")
-    ap.add_argument("--fuse", dest="fuse", action="store_true", default=False)
+    ap.add_argument("--fuse", dest="fuse", action="store_true", default=True)
     ap.add_argument("--no-fuse", dest="fuse", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-unfused", action="store_true", help="skip the per-gate-pass measurement")
+    ap.add_argument("--no-sharded", action="store_true", help="N>1: skip the NCCL-sharded QFT section")
+    ap.add_argument("--sharded-timeout", type=float, default=240.0)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -362,7 +470,8 @@ def main():
     if world > 1:
         import torch
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group("nccl")
+        torch.distributed.init_process_group(
+            "nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
     try:
         return run_qj(args, rank, world)
     finally:

@@ -57,8 +57,9 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--full", nargs="*", default=[])
+    ap.add_argument("--root", default="profiles", help="output root (use /tmp for scratch)")
     a = ap.parse_args()
-    out = os.path.join("profiles", a.tag)
+    out = os.path.join(a.root, a.tag)
     os.makedirs(out, exist_ok=True)
     traffic = {}
     if a.launches:
@@ -109,7 +110,7 @@ def main():
                     for w in want:
                         if w in h:
                             f.write(f"    {w:60s} {row[h.index(w)]} {units[h.index(w)]}\n")
-    with open(os.path.join("profiles", f"ncu_traffic_{a.tag}.json"), "w") as f:
+    with open(os.path.join(a.root, f"ncu_traffic_{a.tag}.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     print("wrote", out)
 
