@@ -9,8 +9,20 @@
 // bit owned by a register index or the loop counter.
 #pragma once
 
+#ifdef __CUDACC_RTC__
+// NVRTC (run-time compiled tile kernels, tile_jit.cpp): no system headers.
+typedef unsigned long long uint64_t;
+typedef unsigned int uint32_t;
+typedef unsigned short uint16_t;
+typedef unsigned char uint8_t;
+typedef long long int64_t;
+typedef short int16_t;
+typedef signed char int8_t;
+typedef int int32_t;
+#else
 #include <cuda_runtime.h>
 #include <stdint.h>
+#endif
 
 namespace qj {
 

@@ -453,54 +453,102 @@ struct MargArgs {
     const void* psi;
 };
 
-// Marginal probabilities: each block bins its part of the state in SMEM
-// (fp64), then adds its bins to the global fp64 bins.  nq <= 12 uses SMEM
-// bins; larger nq uses warp-aggregated global atomics.
+// Marginal fast path: every listed bit lies above the block's contiguous chunk
+// of 2^cb amplitudes, so the whole chunk falls in one bin.  Vectorised loads,
+// fp64 accumulation, block reduction, one atomic per chunk.
+template <typename R>
+__global__ void __launch_bounds__(kThreads) prob_chunk_kernel(const __grid_constant__ MargArgs a, int cb) {
+    using Vec = typename VecT<R>::type;
+    constexpr int V = VecT<R>::V;
+    __shared__ double red[kThreads / 32];
+    const Vec* psi = reinterpret_cast<const Vec*>(a.psi);
+    const uint64_t chunk = blockIdx.x;
+    const uint64_t nvec = 1ull << (cb - V);
+    const uint64_t v0 = chunk * nvec;
+    double acc0 = 0.0, acc1 = 0.0;
+    uint64_t i = threadIdx.x;
+    for (; i + kThreads < nvec; i += 2 * kThreads) {
+        Cx<R> x[1 << V], y[1 << V];
+        unpack(ldv(psi + v0 + i), x);
+        unpack(ldv(psi + v0 + i + kThreads), y);
+#pragma unroll
+        for (int w = 0; w < (1 << V); ++w) {
+            acc0 = fma((double)x[w].re, (double)x[w].re, fma((double)x[w].im, (double)x[w].im, acc0));
+            acc1 = fma((double)y[w].re, (double)y[w].re, fma((double)y[w].im, (double)y[w].im, acc1));
+        }
+    }
+    for (; i < nvec; i += kThreads) {
+        Cx<R> x[1 << V];
+        unpack(ldv(psi + v0 + i), x);
+#pragma unroll
+        for (int w = 0; w < (1 << V); ++w)
+            acc0 = fma((double)x[w].re, (double)x[w].re, fma((double)x[w].im, (double)x[w].im, acc0));
+    }
+    double s = acc0 + acc1;
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+        const uint64_t base = chunk << cb;
+        uint32_t o = 0;
+        for (int q = 0; q < a.nq; ++q) {
+            const uint32_t b = a.pos[q] >= 0 ? (uint32_t)((base >> a.pos[q]) & 1u) : (uint32_t)a.cbit[q];
+            o = (o << 1) | b;
+        }
+        atomicAdd(&a.bins[o], t);
+    }
+}
+
+// Marginal probabilities, general case.  The output bin of index i is
+// assembled from per-byte tables (bin bits contributed by each byte of i).
+// Each thread keeps a running (bin, sum) and flushes it -- to SMEM bins
+// (nq <= 12) or straight to the global fp64 bins -- only when its bin
+// changes: with a grid stride that is a multiple of 2^(max listed bit + 1) a
+// thread's bin never changes, and listed high bits change it rarely.
 template <typename R, bool SMEM>
-__global__ void __launch_bounds__(kThreads) prob_marg_kernel(const __grid_constant__ MargArgs a) {
+__global__ void __launch_bounds__(kThreads) prob_marg_kernel(const __grid_constant__ MargArgs a, int nbytes) {
     __shared__ double sb[SMEM ? 4096 : 1];
+    __shared__ uint32_t tbl[8][256];
     const int nb = 1 << a.nq;
     if constexpr (SMEM) {
         for (int i = threadIdx.x; i < nb; i += blockDim.x) sb[i] = 0.0;
-        __syncthreads();
     }
+    uint32_t cst = 0;  // constant (global) bits of the bin
+    for (int q = 0; q < a.nq; ++q)
+        if (a.pos[q] < 0 && a.cbit[q]) cst |= 1u << (a.nq - 1 - q);
+    for (int e = threadIdx.x; e < nbytes * 256; e += blockDim.x) {
+        const int c = e >> 8, v = e & 255;
+        uint32_t o = c == 0 ? cst : 0u;
+        for (int q = 0; q < a.nq; ++q) {
+            const int p = a.pos[q] - 8 * c;
+            if (a.pos[q] >= 0 && p >= 0 && p < 8 && ((v >> p) & 1)) o |= 1u << (a.nq - 1 - q);
+        }
+        tbl[c][v] = o;
+    }
+    __syncthreads();
     const Cx<R>* psi = reinterpret_cast<const Cx<R>*>(a.psi);
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i0 = start - lane; i0 < a.namp; i0 += stride) {
-        const uint64_t i = i0 + lane;
-        double pr = 0.0;
+    uint32_t cur = 0xffffffffu;
+    double acc = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.namp; i += stride) {
+        const Cx<R> v = psi[i];
         uint32_t o = 0;
-        if (i < a.namp) {
-            const Cx<R> v = psi[i];
-            pr = (double)v.re * (double)v.re + (double)v.im * (double)v.im;
-            for (int q = 0; q < a.nq; ++q) {
-                const uint32_t b = a.pos[q] >= 0 ? (uint32_t)((i >> a.pos[q]) & 1u) : (uint32_t)a.cbit[q];
-                o = (o << 1) | b;
+        for (int c = 0; c < nbytes; ++c) o |= tbl[c][(i >> (8 * c)) & 255];
+        if (o != cur) {
+            if (cur != 0xffffffffu) {
+                if constexpr (SMEM) atomicAdd(&sb[cur], acc);
+                else atomicAdd(&a.bins[cur], acc);
             }
+            cur = o;
+            acc = 0.0;
         }
-        // warp-aggregate lanes that share a bin
-        const unsigned peers = __match_any_sync(0xffffffffu, o);
-        const int leader = __ffs(peers) - 1;
-        double s = pr;
-        // sum over peers: reduce by iterating bits (peers usually all 32 or 1..few)
-        if (peers == 0xffffffffu) {
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        } else {
-            double t = 0.0;
-            unsigned m = peers;
-            while (m) {
-                const int src = __ffs(m) - 1;
-                m &= m - 1;
-                t += __shfl_sync(peers, pr, src);
-            }
-            s = t;
-        }
-        if ((int)lane == leader) {
-            if constexpr (SMEM) atomicAdd(&sb[o], s);
-            else atomicAdd(&a.bins[o], s);
-        }
+        acc = fma((double)v.re, (double)v.re, fma((double)v.im, (double)v.im, acc));
+    }
+    if (cur != 0xffffffffu) {
+        if constexpr (SMEM) atomicAdd(&sb[cur], acc);
+        else atomicAdd(&a.bins[cur], acc);
     }
     if constexpr (SMEM) {
         __syncthreads();
@@ -887,12 +935,23 @@ cudaError_t run_prob_marginal(const void* psi, int nl, const int* pos, const int
     }
     a.bins = bins;
     a.psi = psi;
-    if (nq <= 12) {
-        static const uint64_t cap = max_resident_blocks(prob_marg_kernel<R, true>, kThreads, 0);
-        prob_marg_kernel<R, true><<<grid_for(a.namp, cap), kThreads, 0, st>>>(a);
+    int minpos = 64;
+    for (int i = 0; i < nq; ++i)
+        if (pos[i] >= 0) minpos = std::min(minpos, pos[i]);
+    const int cb = std::min(nl, 16);
+    if (minpos >= cb && cb >= VecT<R>::V + 8) {
+        prob_chunk_kernel<R><<<(unsigned)(1ull << (nl - cb)), kThreads, 0, st>>>(a, cb);
     } else {
-        static const uint64_t cap = max_resident_blocks(prob_marg_kernel<R, false>, kThreads, 0);
-        prob_marg_kernel<R, false><<<grid_for(a.namp, cap), kThreads, 0, st>>>(a);
+        // grid = a power of two so the stride is a multiple of 2^(max listed bit + 1)
+        // whenever that fits (then every thread's bin is fixed)
+        const int nbytes = (nl + 7) / 8;
+        const bool smem = nq <= 12;
+        const uint64_t cap = smem ? max_resident_blocks(prob_marg_kernel<R, true>, kThreads, 0)
+                                  : max_resident_blocks(prob_marg_kernel<R, false>, kThreads, 0);
+        uint64_t g = 1;
+        while (g * 2 <= cap && g * 2 * kThreads <= a.namp) g *= 2;
+        if (smem) prob_marg_kernel<R, true><<<(unsigned)g, kThreads, 0, st>>>(a, nbytes);
+        else prob_marg_kernel<R, false><<<(unsigned)g, kThreads, 0, st>>>(a, nbytes);
     }
     ls.launches++;
     return cudaGetLastError();

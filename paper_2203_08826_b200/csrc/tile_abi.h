@@ -1,0 +1,113 @@
+// tile_abi.h -- parameter / program-buffer layout shared by the host lowering
+// (tile_pass.cu), the ahead-of-time interpreter kernel and the run-time
+// compiled (NVRTC) tile kernels (tile_jit.cpp).  Plain PODs only: this header
+// is also compiled by NVRTC.
+#pragma once
+
+#include "common.cuh"
+
+namespace qj {
+
+#ifndef QJ_TILE_R
+#define QJ_TILE_R 4
+#endif
+constexpr int TILE_W = 12;
+constexpr int TILE_R = QJ_TILE_R;          // register bits per thread (3 or 4)
+constexpr int TILE_T = TILE_W - TILE_R;    // thread-index bits
+constexpr int TILE_THREADS = 1 << TILE_T;
+constexpr int TILE_NREG = 1 << TILE_R;
+constexpr int TILE_TCH = (TILE_T + 3) / 4;  // 4-bit chunks of the thread index
+constexpr int TILE_MINBLOCKS = 2;
+constexpr int TILE_MAXSEG = 8;
+constexpr int TILE_MAXOPS = 160;
+constexpr int TILE_MAXCX = 64;
+constexpr int TILE_MAXRUNS = 96;
+constexpr int TILE_MAXSLOTS = 1024;
+constexpr int TILE_MAXTERMS = 1024;  // planner budget per pass
+constexpr int TILE_MAXMAT = 1024;    // complex entries in the matrix pool
+
+enum TOpType : uint8_t {
+    TO_H = 0,     // Hadamard on R bit a
+    TO_U1 = 1,    // 2x2 matrix (mat) on R bit a
+    TO_U2 = 2,    // 4x4 matrix (mat) on R bits (a = MSB, b)
+    TO_X = 3,     // X on R bit a
+    TO_SWAP = 4,  // SWAP R bits a, b
+    TO_RUN = 5,   // phase run `run`
+};
+
+struct TOp {
+    uint8_t type, a, b;
+    uint8_t cr_mask, cr_val;  // controls on R bits (R-local bit mask / value)
+    uint8_t pad0;
+    uint16_t idx;             // matrix offset (U1/U2) or run index (RUN)
+    int16_t cx;               // index into cx[] (controls on non-R bits), -1 = none
+    uint16_t pad1[3];
+};
+
+struct TSeg {
+    int8_t tbits[TILE_T];  // window-bit index mapped to thread-id bit i
+    int8_t rbits[TILE_R];  // window-bit index mapped to register-index bit j
+    uint16_t op0, op1;     // op range
+};
+
+enum TRunKind : uint8_t { RUN_SLOT = 0, RUN_ANCHOR = 1 };
+
+struct TRunDesc {
+    uint8_t kind;
+    // ---- RUN_SLOT
+    uint8_t ru;          // register bits with CR slots / single-R-bit L terms
+    uint8_t r0one;       // register bits whose value-0 factor is always 1
+    uint8_t has_scalar;  // S / CT / L-scalar contributions exist
+    int16_t s_slot;
+    int16_t ct_slot[TILE_T][2];
+    int16_t cr_slot[4][2];
+    uint16_t l0, l1;  // generic L term range
+    int32_t ta;       // per-thread scalar table (256 complex) offset in fac, -1 none
+    int32_t tb;       // per-thread register-bit pairs (256 x 4 x 2 complex) offset in fac, -1 none
+    int32_t pt;       // uniform register-pattern table (16 complex) offset in fac, -1 none
+    // ---- RUN_ANCHOR
+    uint8_t anc_r;     // 1: anchor is register bit anc, 0: thread bit anc
+    uint8_t anc;
+    uint8_t vmask;     // values of the anchor with terms (bit v)
+    uint8_t tm[2];     // per v: thread bits with factors
+    uint8_t rm[2];     // per v: register bits with factors
+    uint8_t r1only[2]; // per v: register bits whose x=0 factor is 1
+    int16_t aslot[2];  // per v: per-tile slot (C partner bits and anchor-only terms), -1 none
+    uint32_t fac;      // offset of the factor table: [v][T bit][x] (32) then [v][R bit][x] (16)
+    int32_t ft;        // per-thread thread-partner products [v][tid] offset in fac, -1 none
+};
+
+template <typename R>
+struct TTerm {
+    uint64_t cmask, cval;  // predicate over non-R physical bits (L) or C bits (slots)
+    uint8_t rmask, rval;   // R-local pattern (L terms)
+    uint8_t pad[6];
+    Cx<R> f;
+};
+
+struct TSlot {
+    uint32_t t0, t1;  // term range whose product (with tile predicate) fills the slot
+};
+
+// Device program buffer layout of one pass (offsets in bytes from the base).
+struct TileTablesLayout {
+    uint32_t terms, slots, mats, fac;
+};
+
+template <typename R>
+struct TileArgs {
+    void* psi;
+    const unsigned char* tables;  // device program buffer of this pass
+    TileTablesLayout lay;
+    uint64_t ntiles;
+    int nseg, nops, nslots, pad;
+    int wpos[TILE_W];  // ascending physical positions of the window bits
+    TSeg seg[TILE_MAXSEG];
+    uint64_t tph[TILE_MAXSEG][TILE_TCH][16];  // physical offset of thread-id nibbles per segment
+    uint32_t tlo[TILE_MAXSEG][TILE_TCH][16];  // window-local offset of thread-id nibbles
+    TOp ops[TILE_MAXOPS];
+    uint64_t cx[TILE_MAXCX][2];
+    TRunDesc runs[TILE_MAXRUNS];
+};
+
+}  // namespace qj
