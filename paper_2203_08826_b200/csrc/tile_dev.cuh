@@ -46,6 +46,26 @@ __device__ __forceinline__ void op_h(Cx<R> (&v)[TILE_NREG], R s, uint32_t crm, u
     }
 }
 
+// Unscaled Hadamard butterfly (x + y, x - y): the JIT kernels apply the
+// product of the pass's 1/sqrt(2) factors once, at the store.
+template <typename R, int A>
+__device__ __forceinline__ void op_hu(Cx<R> (&v)[TILE_NREG]) {
+#pragma unroll
+    for (int j = 0; j < TILE_NREG / 2; ++j) {
+        const int lo = ((j >> A) << (A + 1)) | (j & ((1 << A) - 1));
+        const int hi = lo | (1 << A);
+        const Cx<R> x = v[lo], y = v[hi];
+        v[lo] = Cx<R>{x.re + y.re, x.im + y.im};
+        v[hi] = Cx<R>{x.re - y.re, x.im - y.im};
+    }
+}
+
+template <typename R>
+__device__ __forceinline__ void scale_all(Cx<R> (&v)[TILE_NREG], R s) {
+#pragma unroll
+    for (int r = 0; r < TILE_NREG; ++r) v[r] = Cx<R>{v[r].re * s, v[r].im * s};
+}
+
 template <typename R, int A, bool C>
 __device__ __forceinline__ void op_u1(Cx<R> (&v)[TILE_NREG], const Cx<R>* m, uint32_t crm, uint32_t crv, bool ok) {
     const Cx<R> m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];

@@ -471,10 +471,11 @@ cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, Tile
     e = cudaEventRecord(stg.ev[k], st);
     if (e != cudaSuccess) return e;
     a->tables = d;
-    const size_t smem = sizeof(Cx<R>) * ((size_t)(1 << TILE_W) + (size_t)std::max(a->nslots, 1));
+    // tile + two slot tables (the JIT kernel double-buffers them across tiles)
+    const size_t smem = sizeof(Cx<R>) * ((size_t)(1 << TILE_W) + 2 * (size_t)std::max(a->nslots, 1));
     static size_t attr = 0;
     if (smem > attr) {
-        const size_t want = sizeof(Cx<R>) * ((size_t)(1 << TILE_W) + TILE_MAXSLOTS);
+        const size_t want = sizeof(Cx<R>) * ((size_t)(1 << TILE_W) + 2 * TILE_MAXSLOTS);
         e = cudaFuncSetAttribute(tile_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
         if (e != cudaSuccess) return e;
         attr = want;
@@ -484,7 +485,7 @@ cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, Tile
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = std::min<uint64_t>(a->ntiles, (uint64_t)sms * TILE_MINBLOCKS);
     std::string jerr;
-    void* jf = tile_jit_function<R>(*a, &jerr, nullptr);
+    void* jf = tile_jit_function<R>(*a, blob.data() + a->lay.mats, &jerr, nullptr);
     if (jf) {
         e = tile_jit_launch(jf, a, (unsigned)grid, smem, st);
     } else {

@@ -350,3 +350,73 @@ def test_nccl_single_rank_state():
     assert p.exitcode == 0
     e_amp, e_marg, e_full, nsh = q.get(timeout=10)
     assert nsh == 1 and e_amp < 1e-12 and e_marg < 1e-12 and e_full < 1e-12
+
+
+# ------------------------------------------------ edge cases
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+def test_empty_circuit_and_tiny_states(dt):
+    rng = np.random.default_rng(9)
+    psi = rand_state(12, rng, dt)
+    x = to_gpu(psi, dt)
+    st = qjp.State(x, basis=None)
+    st.apply_circuit([], fuse=True)
+    st.apply_circuit([], fuse=False)
+    st.sync()
+    assert np.array_equal(x.cpu().numpy(), psi)
+    for n in (1, 2, 3):
+        circ = C.random_circuit(n, 40, n, max_targets=min(3, n), max_controls=1)
+        p0 = rand_state(n, rng, dt)
+        for fuse in (False, True):
+            x = to_gpu(p0, dt)
+            s = qjp.State(x, basis=None)
+            s.apply_circuit(circ.gates, fuse=fuse)
+            s.canonicalize()
+            s.sync()
+            check_close(x.cpu().numpy(), oracle_circuit(circ, p0, dt), dt)
+
+
+@pytest.mark.slow
+def test_qft32_c128_max_size_closed_form():
+    """64 GiB complex128 state (the largest power of two with room to spare on
+    one B200 besides 33 q): fused QFT |x>, sampled against the closed form."""
+    n, x = 32, 0xB5E3C1A7
+    t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(t, basis=x)
+    st.apply_circuit(C.qft(n).gates, fuse=True)
+    p = st.probabilities([0, 1, 2])
+    assert abs(float(p.sum()) - 1) < 1e-10
+    st.canonicalize()
+    st.sync()
+    rng = np.random.default_rng(32)
+    idx = np.unique(np.concatenate([rng.integers(0, 2**n, 1 << 14), [0, 2**n - 1]])).astype(np.int64)
+    got = t[torch.from_numpy(idx).cuda()].cpu().numpy()
+    m = (np.uint64(x) * idx.astype(np.uint64)) % np.uint64(2**n)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * m.astype(np.float64) / 2**n)
+    assert np.max(np.abs(got - exp)) < 1e-12
+    del st, t
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_supremacy32_c64_fused_vs_unfused():
+    """BASELINE config 4 at full size (32 qubits, complex64, 32 GiB): fused and
+    unfused paths agree amplitude by amplitude on a sample (no oracle fits), and
+    the norm is preserved."""
+    circ = C.supremacy(4, 8, 20)
+    n = circ.n
+    rng = np.random.default_rng(4)
+    idx = torch.from_numpy(np.unique(rng.integers(0, 2**n, 1 << 14)).astype(np.int64)).cuda()
+    t = torch.empty(2**n, dtype=torch.complex64, device="cuda")
+    st = qjp.State(t, basis=0)
+    st.apply_circuit(circ.gates, fuse=True)
+    st.canonicalize()
+    norm = float(st.probabilities([0, 1]).double().sum())
+    a = t[idx].cpu().numpy()
+    st.reset(0)
+    st.apply_circuit(circ.gates, fuse=False)
+    st.sync()
+    b = t[idx].cpu().numpy()
+    assert abs(norm - 1) < 1e-4
+    assert np.max(np.abs(a.astype(np.complex128) - b)) < 1e-5
+    del st, t
+    torch.cuda.empty_cache()

@@ -30,7 +30,7 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "nsecon
 KIND = [(r"diag_kernel<\w+, 0>", "diag_table"), (r"diag_kernel<\w+, 1>", "diag_phase"),
         (r"diag_kernel<\w+, 2>", "diag_neg"), (r"gate_warp_kernel<\w+, \d, \d, \d, 0>", "gate_dense"),
         (r"gate_warp_kernel<\w+, \d, \d, \d, 1>", "gate_x"), (r"gate_warp_kernel<\w+, \d, \d, \d, 2>", "gate_swap"),
-        (r"tile_kernel", "tile"), (r"exchange_kernel", "exchange")]
+        (r"tile_kernel|qj_tile_jit", "tile"), (r"exchange_kernel", "exchange")]
 
 
 def kind_of(name):
