@@ -425,6 +425,73 @@ __device__ __forceinline__ void tile_store(const TileArgs<R>& a, int s, const Cx
     }
 }
 
+// Asynchronous prefetch of a tile into the (swizzled) SMEM buffer with the
+// mapping of segment 0, and the matching register load.  The JIT kernels issue
+// the prefetch of tile i+1 right after tile i's last transpose, so its HBM
+// latency overlaps the last segment's compute and the stores.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <typename R>
+__device__ __forceinline__ void tile_prefetch(const TileArgs<R>& a, uint64_t tile, Cx<R>* sm, int tid) {
+    uint64_t tb = tile;
+#pragma unroll
+    for (int i = 0; i < TILE_W; ++i) tb = insert_zero(tb, a.wpos[i]);
+    const TSeg& S = a.seg[0];
+    const uint64_t base = tb | thread_phys(a, 0, tid);
+    const uint32_t bl = swz<R>(thread_loc(a, 0, tid));
+    uint64_t rm[TILE_R];
+    uint32_t sl[TILE_R];
+#pragma unroll
+    for (int j = 0; j < TILE_R; ++j) {
+        rm[j] = 1ull << a.wpos[S.rbits[j]];
+        sl[j] = swz<R>(1u << S.rbits[j]);
+    }
+    const Cx<R>* psi = reinterpret_cast<const Cx<R>*>(a.psi);
+#pragma unroll
+    for (int r = 0; r < TILE_NREG; ++r) {
+        uint64_t x = base;
+        uint32_t y = bl;
+#pragma unroll
+        for (int j = 0; j < TILE_R; ++j)
+            if ((r >> j) & 1) {
+                x |= rm[j];
+                y ^= sl[j];
+            }
+        if constexpr (sizeof(R) == 8) cp_async16(sm + y, psi + x);
+        else cp_async8(sm + y, psi + x);
+    }
+    cp_async_commit();
+}
+
+template <typename R>
+__device__ __forceinline__ void tile_load_prefetched(const TileArgs<R>& a, Cx<R> (&v)[TILE_NREG], const Cx<R>* sm,
+                                                     int tid) {
+    cp_async_wait_all();
+    __syncthreads();
+    const TSeg& S = a.seg[0];
+    const uint32_t bl = swz<R>(thread_loc(a, 0, tid));
+    uint32_t sl[TILE_R];
+#pragma unroll
+    for (int j = 0; j < TILE_R; ++j) sl[j] = swz<R>(1u << S.rbits[j]);
+#pragma unroll
+    for (int r = 0; r < TILE_NREG; ++r) {
+        uint32_t y = bl;
+#pragma unroll
+        for (int j = 0; j < TILE_R; ++j)
+            if ((r >> j) & 1) y ^= sl[j];
+        v[r] = sm[y];
+    }
+}
+
 // Registers of segment s-1 -> swizzled SMEM -> registers of segment s.
 template <typename R>
 __device__ __forceinline__ void tile_transpose(const TileArgs<R>& a, int s, Cx<R> (&v)[TILE_NREG], Cx<R>* sm,
