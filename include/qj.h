@@ -145,6 +145,8 @@ typedef struct {
 } qj_gate;
 
 #define QJ_FUSE 1u       /* plan runs of gates into fused window tile passes */
+#define QJ_FUSE_GATES 2u /* first apply the paper's greedy fusion into <= 2-qubit
+                            dense gates; combinable with QJ_FUSE */
 
 /* Apply `ngates` gates in order.  Without QJ_FUSE every gate is one pass as
  * if issued through the single-gate entry points.  With QJ_FUSE the planner
@@ -242,6 +244,17 @@ typedef struct {
 
 qj_status qj_plan_circuit(int n, int nshards, int amp_bytes, const qj_gate* gates, int ngates,
                           uint32_t flags, qj_plan_step* out, int max_steps, int* nsteps, int* phys);
+
+/* The paper's gate fusion (Table 2 Gates* / Depth*), host
+ * only: greedily combine the circuit into gates of at most `max_qubits` (1 or
+ * 2) qubits.  Fused groups come back as QJ_GATE_DENSE gates whose matrices
+ * (complex128, row-major, first target = MSB) are written to `mats` (caller
+ * buffer of 32 doubles per output gate) and pointed to by `data`; gates on more
+ * qubits are copied unchanged (their `data` still points at the caller's
+ * input).  Gate data are read as complex128.  Errors: as qj_apply_circuit,
+ * CAPACITY if more than max_out gates. */
+qj_status qj_fuse_circuit(int n, const qj_gate* in, int nin, int max_qubits, qj_gate* out, double* mats,
+                          int max_out, int* nout, int* src /* max_out, may be NULL: input index or -1 */);
 
 /* The exchange rule of the multi-GPU layer: for a swap of global bit `gbit`,
  * rank `rank` trades with `*peer` the amplitudes of its shard whose swapped

@@ -558,7 +558,7 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
     if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
     if (ngates < 0) return fail(QJ_ERR_INVALID_ARG, "ngates=%d < 0", ngates);
     if (ngates > 0 && !gates) return fail(QJ_ERR_INVALID_ARG, "gates is NULL");
-    if (flags & ~QJ_FUSE) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    if (flags & ~(QJ_FUSE | QJ_FUSE_GATES)) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
     std::vector<LGate> gs((size_t)ngates);
     for (int i = 0; i < ngates; ++i) {
         const qj_gate& g = gates[i];
@@ -570,6 +570,7 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
             return st;
         }
     }
+    if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, s->n, 2);
     return apply_lgates(s, gs, (flags & QJ_FUSE) != 0);
 }
 
@@ -653,6 +654,49 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
     });
     if (e != cudaSuccess) return cuda_fail(e, "bins launch");
     s->ctr.launches = s->ls.launches;
+    return QJ_OK;
+}
+
+qj_status qj_fuse_circuit(int n, const qj_gate* in, int nin, int max_qubits, qj_gate* out, double* mats, int max_out,
+                          int* nout, int* src) {
+    if (!nout || (nin > 0 && !in) || (max_out > 0 && (!out || !mats))) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
+    if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
+    if (max_qubits < 1 || max_qubits > 2) return fail(QJ_ERR_UNSUPPORTED, "max_qubits must be 1 or 2 (got %d)", max_qubits);
+    qj_state_s tmp;
+    tmp.n = n;
+    tmp.dt = QJ_C128;
+    std::vector<LGate> gs((size_t)nin);
+    for (int i = 0; i < nin; ++i) {
+        const qj_gate& q = in[i];
+        if (q.nt > QJ_MAX_TARGETS || q.nc > QJ_MAX_CONTROLS)
+            return fail(QJ_ERR_TOO_MANY_TARGETS, "gate %d: nt=%d nc=%d exceeds the limits", i, q.nt, q.nc);
+        qj_status st = make_lgate(&tmp, q.kind, q.targets, q.nt, q.controls, q.nc, q.data, gs[(size_t)i]);
+        if (st != QJ_OK) return st;
+    }
+    std::vector<LGate> fused = fuse_gates(gs, n, max_qubits);
+    if ((int)fused.size() > max_out) return fail(QJ_ERR_CAPACITY, "%zu fused gates > %d", fused.size(), max_out);
+    for (size_t i = 0; i < fused.size(); ++i) {
+        if (src) src[i] = fused[i].src;
+        const LGate& f = fused[i];
+        qj_gate& o = out[i];
+        std::memset(&o, 0, sizeof(o));
+        o.kind = f.kind;
+        o.nt = f.nt;
+        o.nc = f.nc;
+        for (int j = 0; j < f.nt; ++j) o.targets[j] = f.t[j];
+        for (int j = 0; j < f.nc; ++j) o.controls[j] = f.c[j];
+        if (f.src >= 0) {  // a gate copied unchanged
+            o.data = in[f.src].data;
+        } else {
+            double* m = mats + 32 * i;
+            for (size_t j = 0; j < f.data.size(); ++j) {
+                m[2 * j] = f.data[j].real();
+                m[2 * j + 1] = f.data[j].imag();
+            }
+            o.data = m;
+        }
+    }
+    *nout = (int)fused.size();
     return QJ_OK;
 }
 

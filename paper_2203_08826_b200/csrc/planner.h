@@ -26,6 +26,7 @@ struct LGate {
     int t[QJ_MAX_TARGETS] = {};
     int c[QJ_MAX_CONTROLS] = {};
     std::vector<cd> data;  // dense 4^nt / diag 2^nt / fsim 5
+    int src = -1;          // fusion: index of the input gate this one is (-1: fused group)
 };
 
 struct Step {
@@ -50,6 +51,10 @@ class Planner {
     void plan_gate(const PlanContext& ctx, const LGate& g, std::vector<Step>& out);
     void plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates, std::vector<Step>& out);
 };
+
+// The paper's greedy gate fusion into gates of <= max_qubits qubits
+// (fusion.cpp).
+std::vector<LGate> fuse_gates(const std::vector<LGate>& gates, int n, int max_qubits);
 
 // Pass specialisation of one logical gate on local physical positions, as
 // seen from shard `r` (global bits fixed to r's bits).  Returns false when

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libqj.so")
 QJ_C64, QJ_C128 = 0, 1
 QJ_KEEP = (1 << 64) - 1
 QJ_FUSE = 1
+QJ_FUSE_GATES = 2
 MAX_TARGETS, MAX_CONTROLS = 8, 16
 KIND = {"dense": 0, "x": 1, "z": 2, "swap": 3, "fsim": 4, "diag": 5}
 STATUS = {0: "QJ_OK", 1: "QJ_ERR_INVALID_ARG", 2: "QJ_ERR_INDEX_OUT_OF_RANGE",
@@ -30,7 +31,7 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_apply_diagonal", "qj_apply_circuit", "qj_probabilities", "qj_sync",
            "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
            "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
-           "qj_plan_circuit", "qj_exchange_peer"]
+           "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit"]
 
 
 class QJError(RuntimeError):
@@ -103,6 +104,8 @@ def lib():
         "qj_plan_circuit": ([I, I, I, ctypes.POINTER(qj_gate), I, ctypes.c_uint32, ctypes.POINTER(qj_plan_step), I,
                              IP, IP], S),
         "qj_exchange_peer": ([I, I, IP, IP], None),
+        "qj_fuse_circuit": ([I, ctypes.POINTER(qj_gate), I, I, ctypes.POINTER(qj_gate), ctypes.POINTER(ctypes.c_double),
+                             I, IP, IP], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -184,6 +187,44 @@ def plan_circuit(n, nshards, gates, fuse=False, amp_bytes=16, max_steps=1 << 16)
                       "fix": [(o.fpos[j], o.fval[j]) for j in range(o.nfix)], "touch": o.touch, "m": m,
                       "gbit": o.gbit, "lbit": o.lbit, "alg_bytes": o.alg_bytes})
     return steps, list(phys)
+
+
+class FusedGate:
+    """A gate returned by fuse_circuit (dense matrix on `targets`, or an input
+    gate passed through unchanged)."""
+
+    def __init__(self, kind, targets, controls, matrix):
+        self.kind, self.targets, self.controls = kind, tuple(targets), tuple(controls)
+        self.m = matrix
+        self.data = (matrix,) if kind in ("dense", "diag") else ()
+
+    @property
+    def qubits(self):
+        return self.targets + self.controls
+
+
+def fuse_circuit(n, gates, max_qubits=2):
+    """The paper's greedy gate fusion run by the library:
+    returns the fused gate list (FusedGate for fused groups; the original gate
+    objects for gates passed through)."""
+    gates = list(gates)
+    arr, ng, keep = pack_gates(gates)
+    out = (qj_gate * max(1, ng))()
+    mats = (ctypes.c_double * (32 * max(1, ng)))()
+    cnt = ctypes.c_int()
+    src = (ctypes.c_int * max(1, ng))()
+    _check(lib().qj_fuse_circuit(n, arr, ng, max_qubits, out, mats, ng, ctypes.byref(cnt), src))
+    res = []
+    for i in range(cnt.value):
+        o = out[i]
+        if src[i] >= 0:
+            res.append(gates[src[i]])      # passed through unchanged
+        else:
+            k = o.nt
+            m = np.array(mats[32 * i:32 * i + 2 * 4 ** k]).view(np.complex128).reshape(2 ** k, 2 ** k)
+            res.append(FusedGate("dense", o.targets[:o.nt], o.controls[:o.nc], m))
+    del keep
+    return res
 
 
 class State:
@@ -322,9 +363,12 @@ class State:
         workloads.gates.Gate) into a qj_gate array; returns (array, n, keepalive)."""
         return pack_gates(gates, self.np_dtype)
 
-    def apply_circuit(self, gates, fuse=False, packed=None):
+    def apply_circuit(self, gates, fuse=False, packed=None, fuse_gates=False):
+        """fuse: window tile passes (QJ_FUSE); fuse_gates: first the paper's
+        greedy <= 2-qubit fusion (QJ_FUSE_GATES)."""
         arr, ng, keep = packed if packed is not None else self.pack_circuit(gates)
-        _check(lib().qj_apply_circuit(self._h, arr, ng, QJ_FUSE if fuse else 0))
+        flags = (QJ_FUSE if fuse else 0) | (QJ_FUSE_GATES if fuse_gates else 0)
+        _check(lib().qj_apply_circuit(self._h, arr, ng, flags))
         del keep
 
     # -- readout -----------------------------------------------------------

@@ -178,10 +178,10 @@ def test_circuits_vs_oracle(dt, name):
     n = circ.n
     rng = np.random.default_rng(11)
     psi = rand_state(n, rng, dt)
-    for fuse in (False, True):
+    for fuse, fg in ((False, False), (True, False), (False, True), (True, True)):
         x = to_gpu(psi, dt)
         st = qjp.State(x, basis=None)
-        st.apply_circuit(circ.gates, fuse=fuse)
+        st.apply_circuit(circ.gates, fuse=fuse, fuse_gates=fg)
         pf = st.probabilities([0, n - 1]).cpu().numpy()  # canonical through the map
         st.canonicalize()
         st.sync()
