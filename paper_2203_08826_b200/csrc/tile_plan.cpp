@@ -52,7 +52,23 @@ struct PassBuild {
     std::vector<Step> singles;  // each gate as a single-gate pass, converted at admission
     uint64_t W = 0;
     int nops = 0, nmat = 0, nterms = 0, nnd = 0;  // nnd: non-diagonal ops (each may flush one run)
+    double cost = 0;                               // estimated arithmetic per amplitude
 };
+
+// Estimated arithmetic per amplitude of a tile op (FP operations; a flushed
+// phase run before a non-diagonal op adds ~1 complex multiply), used to keep a
+// pass's compute within its HBM time.
+double op_cost(const HOp& op) {
+    switch (op.type) {
+        case TO_X:
+        case TO_SWAP: return 1 + 4;
+        case TO_U2: return 16 + 4;
+        default: break;
+    }
+    const bool h = op.m.size() == 4 && op.cmask == 0 && op.m[0] == op.m[1] && op.m[0] == op.m[2] &&
+                   op.m[3] == -op.m[0] && op.m[0].imag() == 0;
+    return h ? 2 + 4 : 8 + 4;
+}
 
 // Phase terms of a diagonal gate on physical positions.
 bool diag_terms(const LGate& g, const std::vector<int>& phys, std::vector<HTerm>& out) {
@@ -284,46 +300,91 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
         else s.alg_bytes = pass_alg_bytes(s.pass, ctx.nl, ctx.amp_bytes);
         return s;
     };
-    for (const LGate& g : gates) {
-        if (g.kind == QJ_GATE_SWAP && g.nc == 0) {
-            // relabel: the two logical qubits exchange physical bits
-            const int a = g.t[0], b = g.t[1];
-            std::swap(phys[a], phys[b]);
-            continue;
-        }
-        Item it;
-        std::vector<HTerm> terms;
-        if (diag_terms(g, phys, terms)) {
-            it.diag = true;
-            it.terms = std::move(terms);
-            if (pb.nterms + (int)it.terms.size() > max_terms - 8) close();
-            pb.nterms += (int)it.terms.size();
+    // DAG-aware packing: a gate that does not fit the current pass is deferred
+    // and blocks its qubits; later gates that depend on no deferred gate keep
+    // joining the pass (they commute with everything deferred).  Deferred
+    // gates start the next pass, in program order.
+    std::vector<int> remaining(gates.size());
+    for (size_t i = 0; i < gates.size(); ++i) remaining[i] = (int)i;
+    std::vector<char> blocked(ctx.n, 0);
+    double budget = ctx.amp_bytes == 16 ? 96.0 : 96.0;
+    if (const char* b = getenv("QJ_TILE_BUDGET")) budget = atof(b);
+    const bool dag = !(getenv("QJ_TILE_DAG") && getenv("QJ_TILE_DAG")[0] == '0');
+    while (!remaining.empty()) {
+        std::vector<int> deferred;
+        std::fill(blocked.begin(), blocked.end(), 0);
+        auto defer = [&](int idx) {
+            deferred.push_back(idx);
+            const LGate& g = gates[idx];
+            for (int i = 0; i < g.nt; ++i) blocked[g.t[i]] = 1;
+            for (int i = 0; i < g.nc; ++i) blocked[g.c[i]] = 1;
+        };
+        for (int idx : remaining) {
+            const LGate& g = gates[idx];
+            bool blk = false;
+            for (int i = 0; i < g.nt; ++i) blk |= blocked[g.t[i]] != 0;
+            for (int i = 0; i < g.nc; ++i) blk |= blocked[g.c[i]] != 0;
+            if (blk) {
+                defer(idx);
+                continue;
+            }
+            if (g.kind == QJ_GATE_SWAP && g.nc == 0) {
+                // relabel: the two logical qubits exchange physical bits
+                std::swap(phys[g.t[0]], phys[g.t[1]]);
+                continue;
+            }
+            Item it;
+            std::vector<HTerm> terms;
+            if (diag_terms(g, phys, terms)) {
+                if (pb.nterms + (int)terms.size() > max_terms - 8 || pb.cost + 0.05 > budget) {
+                    defer(idx);
+                    continue;
+                }
+                it.diag = true;
+                it.terms = std::move(terms);
+                pb.nterms += (int)it.terms.size();
+                pb.cost += 0.05 * (double)it.terms.size();
+                pb.items.push_back(std::move(it));
+                pb.singles.push_back(single(g));
+                continue;
+            }
+            HOp op;
+            if (!make_op(g, phys, op)) {
+                // not fusable: runs alone once nothing earlier is pending
+                if (pb.items.empty() && deferred.empty()) {
+                    plan_gate(ctx, g, out);
+                } else {
+                    defer(idx);
+                }
+                continue;
+            }
+            uint64_t tm = 0;
+            for (int i = 0; i < g.nt; ++i) tm |= 1ull << op.t[i];
+            const int nm = (int)op.m.size();
+            const double c = op_cost(op);
+            const bool fits = popc(pb.W | tm) <= TILE_W && pb.nops + 2 <= kMaxOpsPerPass &&
+                              pb.nmat + nm <= kMaxMatPerPass && pb.nnd + 1 < TILE_MAXRUNS &&
+                              (pb.cost + c <= budget || pb.items.empty());
+            if (!fits) {
+                defer(idx);
+                if (!dag) {  // sequential packing: everything after waits for the next pass
+                    for (int q = 0; q < ctx.n; ++q) blocked[q] = 1;
+                }
+                continue;
+            }
+            pb.cost += c;
+            pb.W |= tm;
+            pb.nops += 2;  // the op plus a possible run flush before it
+            pb.nnd += 1;
+            pb.nmat += nm;
+            it.op = std::move(op);
+            it.tmask = tm;
             pb.items.push_back(std::move(it));
             pb.singles.push_back(single(g));
-            continue;
         }
-        HOp op;
-        if (!make_op(g, phys, op)) {
-            close();
-            plan_gate(ctx, g, out);
-            continue;
-        }
-        uint64_t tm = 0;
-        for (int i = 0; i < g.nt; ++i) tm |= 1ull << op.t[i];
-        const int nm = (int)op.m.size();
-        const bool fits = popc(pb.W | tm) <= TILE_W && pb.nops + 2 <= kMaxOpsPerPass &&
-                          pb.nmat + nm <= kMaxMatPerPass && pb.nnd + 1 < TILE_MAXRUNS;
-        if (!fits) close();
-        pb.W |= tm;
-        pb.nops += 2;  // the op plus a possible run flush before it
-        pb.nnd += 1;
-        pb.nmat += nm;
-        it.op = std::move(op);
-        it.tmask = tm;
-        pb.items.push_back(std::move(it));
-        pb.singles.push_back(single(g));
+        close();
+        remaining.swap(deferred);
     }
-    close();
 }
 
 }  // namespace qj
