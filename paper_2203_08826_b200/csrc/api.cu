@@ -59,6 +59,18 @@ struct qj_state_s {
     void* xbuf = nullptr;  // exchange staging ring
     size_t xbuf_bytes = 0;
     int total_shards() const { return comm ? nranks : (int)shards.size(); }
+    // circuits seen before: plan + prepared tile passes (+ a CUDA graph)
+    struct CachedPlan {
+        std::vector<uint64_t> key;
+        std::vector<Step> steps;
+        std::vector<int> phys_after;
+        std::vector<PreparedTile> tiles;  // one per TILE step, in order
+        cudaGraphExec_t exec = nullptr;
+        bool graphable = true;
+        uint64_t uses = 0, kernels = 0;
+    };
+    std::vector<CachedPlan*> plans;  // most recent first
+    bool cache_on = true;
     // profiling: event pairs around passes
     bool profiling = false;
     struct Rec {
@@ -333,6 +345,180 @@ qj_status apply_lgates(qj_state s, const std::vector<LGate>& gates, bool fuse) {
     return execute(s, steps);
 }
 
+// ---- plan cache ---------------------------------------------------------
+// The key is the exact request: flags, the qubit map at entry and every gate
+// (kind, qubits, data bit patterns).  A hit skips planning, lowering and the
+// tile program uploads; from the second use on the launches are replayed as a
+// CUDA graph (one launch per circuit).
+std::vector<uint64_t> plan_key(qj_state s, const qj_gate* gates, int ngates, uint32_t flags) {
+    std::vector<uint64_t> k;
+    k.reserve(8 + (size_t)ngates * 12);
+    k.push_back(flags);
+    k.push_back((uint64_t)s->n);
+    for (int q = 0; q < s->n; ++q) k.push_back((uint64_t)s->phys[q]);
+    k.push_back((uint64_t)ngates);
+    for (int i = 0; i < ngates; ++i) {
+        const qj_gate& g = gates[i];
+        k.push_back(((uint64_t)g.kind << 40) | ((uint64_t)g.nt << 20) | (uint64_t)g.nc);
+        uint64_t w = 0;
+        for (int j = 0; j < g.nt; ++j) w = (w << 6) | (uint64_t)g.targets[j];
+        k.push_back(w);
+        w = 0;
+        for (int j = 0; j < g.nc; ++j) w = (w << 6) | (uint64_t)g.controls[j];
+        k.push_back(w);
+        size_t cnt = 0;
+        if (g.kind == QJ_GATE_DENSE) cnt = (size_t)1 << (2 * g.nt);
+        else if (g.kind == QJ_GATE_DIAG) cnt = (size_t)1 << g.nt;
+        else if (g.kind == QJ_GATE_FSIM) cnt = 5;
+        const size_t words = cnt * (size_t)s->amp_bytes / 8;
+        const uint64_t* p = static_cast<const uint64_t*>(g.data);
+        for (size_t j = 0; j < words; ++j) {
+            uint64_t v;
+            std::memcpy(&v, p + j, 8);
+            k.push_back(v);
+        }
+    }
+    return k;
+}
+
+void release_plan(qj_state_s::CachedPlan* p) {
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    for (auto& t : p->tiles) tile_release(t);
+    delete p;
+}
+
+qj_status run_cached(qj_state s, qj_state_s::CachedPlan& p) {
+    cudaError_t e = cudaSuccess;
+    size_t ti = 0;
+    for (const Step& st : p.steps) {
+        if (st.type == Step::EXCHANGE) {
+            for (size_t r = 0; r < s->shards.size(); ++r) {
+                if ((r >> st.gbit) & 1) continue;
+                const size_t r2 = r | (1ull << st.gbit);
+                e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return run_exchange<R>(s->shards[r], s->shards[r2], s->nl, st.lbit, s->stream, s->ls);
+                });
+                if (e != cudaSuccess) return cuda_fail(e, "exchange launch");
+            }
+            continue;
+        }
+        ProfScope prof(s, st.type == Step::TILE ? PROF_TILE : st.pass.kind, st.alg_bytes);
+        if (st.type == Step::TILE) {
+            e = tile_launch_prepared(p.tiles[ti++], s->stream, s->ls);
+        } else {
+            void* ptr = shard_ptr(s, st.shard);
+            e = by_dtype(s->dt, [&](auto z) {
+                using R = decltype(z);
+                return run_pass<R>(st.pass, ptr, s->nl, s->stream, s->scratch, s->scratch_bytes, s->ls);
+            });
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cached pass launch");
+    }
+    return QJ_OK;
+}
+
+void account(qj_state s, const qj_state_s::CachedPlan& p) {
+    for (const Step& st : p.steps) {
+        if (st.type == Step::EXCHANGE) {
+            s->ctr.exchanges++;
+            s->ctr.exchange_bytes += (double)s->amp_bytes * (double)(1ull << (s->nl - 1)) * (double)s->shards.size();
+        } else {
+            s->ctr.passes++;
+            s->ctr.alg_bytes += st.alg_bytes;
+        }
+    }
+}
+
+// Returns QJ_OK with *done = false when the request is not cacheable.
+qj_status apply_circuit_cached(qj_state s, const qj_gate* gates, int ngates, uint32_t flags,
+                               const std::vector<LGate>& gs, bool* done) {
+    *done = false;
+    if (!s->cache_on || s->comm) return QJ_OK;
+    std::vector<uint64_t> key = plan_key(s, gates, ngates, flags);
+    for (size_t i = 0; i < s->plans.size(); ++i) {
+        qj_state_s::CachedPlan* p = s->plans[i];
+        if (p->key != key) continue;
+        std::rotate(s->plans.begin(), s->plans.begin() + (long)i, s->plans.begin() + (long)i + 1);
+        const uint64_t before = s->ls.launches;
+        const bool graph_ok = p->graphable && !s->profiling && s->stream != nullptr;
+        if (graph_ok && !p->exec && p->uses >= 1) {
+            cudaGraph_t g = nullptr;
+            cudaError_t e = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal);
+            if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+            qj_status q = run_cached(s, *p);
+            e = cudaStreamEndCapture(s->stream, &g);
+            if (q != QJ_OK) return q;
+            if (e != cudaSuccess) return cuda_fail(e, "graph capture end");
+            e = cudaGraphInstantiate(&p->exec, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) {
+                p->exec = nullptr;
+                p->graphable = false;
+                cudaGetLastError();
+                return cuda_fail(e, "graph instantiate");
+            }
+            s->ls.launches = before;  // captured, not run
+        }
+        if (graph_ok && p->exec) {
+            cudaError_t e = cudaGraphLaunch(p->exec, s->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+            s->ls.launches += p->kernels;
+        } else {
+            if (qj_status q = run_cached(s, *p)) return q;
+        }
+        p->uses++;
+        account(s, *p);
+        s->phys = p->phys_after;
+        s->ctr.launches = s->ls.launches;
+        *done = true;
+        return QJ_OK;
+    }
+    // miss: plan, prepare the tile passes, run, remember
+    auto* p = new qj_state_s::CachedPlan;
+    p->key.swap(key);
+    PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, s->total_shards(), &s->phys};
+    s->planner.plan(ctx, gs, (flags & QJ_FUSE) != 0, p->steps);
+    for (const Step& st : p->steps) {
+        if (st.type == Step::TILE) {
+            PreparedTile t;
+            cudaError_t e = by_dtype(s->dt, [&](auto z) {
+                using R = decltype(z);
+                return tile_prepare<R>(st.tile, shard_ptr(s, st.shard), s->nl, t);
+            });
+            if (e != cudaSuccess) {
+                release_plan(p);
+                return cuda_fail(e, "tile prepare");
+            }
+            p->tiles.push_back(std::move(t));
+        } else if (st.type == Step::PASS && st.pass.k > 5 && st.pass.kind == PK_DENSE) {
+            p->graphable = false;  // big-k passes stage their matrix with a host copy
+            const size_t need = (size_t)s->amp_bytes * ((size_t)1 << (2 * st.pass.k));
+            if (qj_status q = ensure_scratch(s, need)) {
+                release_plan(p);
+                return q;
+            }
+        }
+    }
+    p->phys_after = s->phys;
+    const uint64_t before = s->ls.launches;
+    if (qj_status q = run_cached(s, *p)) {
+        release_plan(p);
+        return q;
+    }
+    p->kernels = s->ls.launches - before;
+    p->uses = 1;
+    account(s, *p);
+    s->ctr.launches = s->ls.launches;
+    s->plans.insert(s->plans.begin(), p);
+    if (s->plans.size() > 16) {
+        release_plan(s->plans.back());
+        s->plans.pop_back();
+    }
+    *done = true;
+    return QJ_OK;
+}
+
 }  // namespace
 
 // ===================================================================== ABI
@@ -482,6 +668,8 @@ qj_status qj_state_free(qj_state s) {
     }
     for (auto ev : s->pool) cudaEventDestroy(ev);
     s->stg.release();
+    for (auto* p : s->plans) release_plan(p);
+    s->plans.clear();
     if (s->scratch) cudaFree(s->scratch);
     if (s->bins) cudaFree(s->bins);
     if (s->xbuf) cudaFree(s->xbuf);
@@ -571,6 +759,9 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
         }
     }
     if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, s->n, 2);
+    bool done = false;
+    if (qj_status st = apply_circuit_cached(s, gates, ngates, flags, gs, &done)) return st;
+    if (done) return QJ_OK;
     return apply_lgates(s, gs, (flags & QJ_FUSE) != 0);
 }
 

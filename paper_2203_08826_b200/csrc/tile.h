@@ -73,6 +73,22 @@ struct TileStaging {
 template <typename R>
 cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, TileStaging& stg, LaunchStats& ls);
 
+// A tile pass lowered once with a persistent device program buffer, for
+// cached circuits replayed (and captured into CUDA graphs) without re-lowering
+// or host->device copies.
+struct PreparedTile {
+    std::vector<unsigned char> args;  // TileArgs<R> bytes (tables -> dev)
+    void* dev = nullptr;              // device program buffer (owned)
+    void* jit = nullptr;              // JIT function or nullptr (interpreter)
+    size_t smem = 0;
+    unsigned grid = 0;
+    int amp_bytes = 16;
+};
+template <typename R>
+cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out);
+cudaError_t tile_launch_prepared(const PreparedTile& p, cudaStream_t st, LaunchStats& ls);
+void tile_release(PreparedTile& p);
+
 // Whether a planned pass lowers within the kernel's capacities.
 bool tile_fits(const TileSpec& t, int nl, int amp_bytes);
 

@@ -499,6 +499,60 @@ cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, Tile
     return e;
 }
 
+template <typename R>
+cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out) {
+    static TileArgs<R>* a = new TileArgs<R>;
+    std::vector<unsigned char> blob;
+    if (!lower_tile<R>(t, nl, a, blob)) return cudaErrorInvalidValue;
+    a->psi = psi;
+    out.amp_bytes = (int)(2 * sizeof(R));
+    if (!blob.empty()) {
+        cudaError_t e = cudaMalloc(&out.dev, blob.size());
+        if (e != cudaSuccess) return e;
+        e = cudaMemcpy(out.dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return e;
+    }
+    a->tables = static_cast<const unsigned char*>(out.dev);
+    out.smem = sizeof(Cx<R>) * ((size_t)(1 << TILE_W) + 2 * (size_t)std::max(a->nslots, 1));
+    static size_t attr = 0;
+    if (out.smem > attr) {
+        const size_t want = sizeof(Cx<R>) * ((size_t)(1 << TILE_W) + 2 * TILE_MAXSLOTS);
+        cudaError_t e = cudaFuncSetAttribute(tile_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+        if (e != cudaSuccess) return e;
+        attr = want;
+    }
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    out.grid = (unsigned)std::min<uint64_t>(a->ntiles, (uint64_t)sms * TILE_MINBLOCKS);
+    std::string jerr;
+    out.jit = tile_jit_function<R>(*a, blob.empty() ? nullptr : blob.data() + a->lay.mats, &jerr, nullptr);
+    out.args.assign(reinterpret_cast<unsigned char*>(a), reinterpret_cast<unsigned char*>(a) + sizeof(TileArgs<R>));
+    return cudaSuccess;
+}
+
+cudaError_t tile_launch_prepared(const PreparedTile& p, cudaStream_t st, LaunchStats& ls) {
+    cudaError_t e;
+    if (p.jit) {
+        e = tile_jit_launch(p.jit, p.args.data(), p.grid, p.smem, st);
+    } else if (p.amp_bytes == 16) {
+        tile_kernel<double><<<p.grid, TILE_THREADS, p.smem, st>>>(*reinterpret_cast<const TileArgs<double>*>(p.args.data()));
+        e = cudaGetLastError();
+    } else {
+        tile_kernel<float><<<p.grid, TILE_THREADS, p.smem, st>>>(*reinterpret_cast<const TileArgs<float>*>(p.args.data()));
+        e = cudaGetLastError();
+    }
+    ls.launches++;
+    return e;
+}
+
+void tile_release(PreparedTile& p) {
+    if (p.dev) cudaFree(p.dev);
+    p.dev = nullptr;
+}
+
+template cudaError_t tile_prepare<float>(const TileSpec&, void*, int, PreparedTile&);
+template cudaError_t tile_prepare<double>(const TileSpec&, void*, int, PreparedTile&);
 template cudaError_t run_tile<float>(const TileSpec&, void*, int, cudaStream_t, TileStaging&, LaunchStats&);
 template cudaError_t run_tile<double>(const TileSpec&, void*, int, cudaStream_t, TileStaging&, LaunchStats&);
 

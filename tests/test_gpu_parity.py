@@ -420,3 +420,31 @@ def test_supremacy32_c64_fused_vs_unfused():
     assert np.max(np.abs(a.astype(np.complex128) - b)) < 1e-5
     del st, t
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------ plan cache + CUDA graph replay
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("fuse", [False, True])
+def test_plan_cache_graph_replay(dt, fuse):
+    """The same circuit applied repeatedly on one handle: 1st call plans, 2nd
+    captures a CUDA graph, later calls replay it (non-default stream)."""
+    n = 16
+    circ = C.random_circuit(n, 150, 77, max_targets=2, max_controls=1)
+    circ.gates += C.qft(n).gates
+    rng = np.random.default_rng(12)
+    psi = rand_state(n, rng, dt)
+    stream = torch.cuda.Stream()
+    x = to_gpu(psi, dt)
+    torch.cuda.synchronize()
+    st = qjp.State(x, basis=None, stream=stream)
+    packed = st.pack_circuit(circ.gates)
+    exp = psi.astype(np.complex128)
+    mats = [gate_matrix_for(g, dt) for g in circ.gates]
+    for rep in range(4):
+        st.apply_circuit(None, fuse=fuse, packed=packed)
+        exp = oracle.run(circ, exp, mats)
+    pf = st.probabilities([0, 5, n - 1]).cpu().numpy()
+    st.canonicalize()
+    st.sync()
+    check_close(x.cpu().numpy(), exp, dt)
+    assert np.max(np.abs(pf - oracle.probabilities(exp, n, [0, 5, n - 1]))) < TOL[dt]

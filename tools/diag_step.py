@@ -6,13 +6,15 @@ import torch
 import paper_2203_08826_b200 as qj
 from workloads import circuits as C
 
+WL = os.environ.get("WL", "qft")
 n = int(os.environ.get("N", 30))
 fuse = os.environ.get("FUSE", "1") == "1"
 dev = torch.device("cuda", 0)
 s = torch.cuda.Stream(dev)
 psi = torch.empty(1 << n, dtype=torch.complex128, device=dev)
 st = qj.State(psi, basis=None, stream=s)
-packed = st.pack_circuit(C.qft(n).gates)
+circ = C.qft(n) if WL == "qft" else C.variational(n, layers=20)
+packed = st.pack_circuit(circ.gates)
 pb = torch.empty(1024, dtype=torch.float64, device=dev)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 for it in range(4):
