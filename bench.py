@@ -189,7 +189,7 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------- qj arm
-def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True):
+def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_gates=False):
     """Time `steps` steps (state reset + circuit + 10-qubit marginal) on the
     device with CUDA events; returns timings, per-kind profile and counters."""
     n = wl["n"]
@@ -203,7 +203,7 @@ def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True):
 
     def step():
         st.reset(wl["basis"])
-        st.apply_circuit(None, fuse=fuse, packed=packed)
+        st.apply_circuit(None, fuse=fuse, packed=packed, fuse_gates=fuse_gates)
         st.probabilities(readout, out=pbuf)
 
     def barrier():
@@ -412,6 +412,22 @@ def run_qj(args, rank, world):
         del u
         torch.cuda.empty_cache()
 
+    # ---- the paper's own fusion: greedy <= 2-qubit dense
+    # gates, then one pass per fused gate (row f1 of SURVEY 8(f))
+    paper = None
+    if args.fuse and not args.no_unfused:
+        pf = measure(qj, torch, wl, False, max(1, min(steps, 3)), 1, dev, world, fuse_gates=True)
+        ps = max(1, min(steps, 3))
+        pb = pf["ctr"]["alg_bytes"] / ps
+        paper = {"value": pf["ms_max"] / 1e3 / (ps * world), "unit": "s/circuit", "steps": ps,
+                 "passes_per_circuit": pf["ctr"]["passes"] / ps,
+                 "effective_gbs": pb / (pf["ms_max"] / ps / 1e3) / 1e9,
+                 "effective_frac": pb / (pf["ms_max"] / ps / 1e3) / 1e9 / peak,
+                 "roofline": roofline_of(pf["prof"], pf["ms_prof"], peak, peak_src, traffic, traffic_src)}
+        pf["st"].free()
+        del pf
+        torch.cuda.empty_cache()
+
     ms_max = m["ms_max"]
     value = ms_max / 1e3 / (steps * world)
     per_step_bytes = m["ctr"]["alg_bytes"] / steps
@@ -440,6 +456,7 @@ def run_qj(args, rank, world):
         "kinds": kinds_of(m["prof"], steps, peak),
         "profiled_ms_per_step": m["ms_prof"] / steps,
         "unfused": unfused,
+        "paper_fusion": paper,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_ms / 1e3 / (steps * world), "unit": "s/circuit",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -448,3 +448,40 @@ def test_plan_cache_graph_replay(dt, fuse):
     st.sync()
     check_close(x.cpu().numpy(), exp, dt)
     assert np.max(np.abs(pf - oracle.probabilities(exp, n, [0, 5, n - 1]))) < TOL[dt]
+
+
+# ------------------------------------------------ f3: Trotterized adiabatic TFIM
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("n,periodic", [(10, True), (13, False), (2, True)])
+def test_tfim_trotter_vs_oracle(dt, n, periodic):
+    """The Trotter circuit of the adiabatic TFIM run through
+    the library (unfused, fused tile pass, paper fusion) vs the gate oracle."""
+    from workloads import evolution as W
+    circ = W.adiabatic_circuit(n, 1.0, 0.05, periodic=periodic)
+    psi = np.zeros(2**n, dtype=dt)
+    psi[0] = 1
+    exp = oracle_circuit(circ, psi, dt)
+    for fuse, fg in ((False, False), (True, False), (True, True)):
+        x = torch.empty(2**n, dtype=TDT[dt], device="cuda")
+        st = qjp.State(x, basis=0)
+        st.apply_circuit(circ.gates, fuse=fuse, fuse_gates=fg)
+        st.canonicalize()
+        st.sync()
+        check_close(x.cpu().numpy(), exp, dt)
+
+
+def test_tfim_adiabatic_ground_energy_gpu():
+    """n = 8, T = 20, dt = 0.05 on the GPU: <H1> within 2% of the exact ground
+    energy of the dense oracle's H1 (SPEC S:576 at a larger n)."""
+    from oracle import evolution as E
+    from workloads import evolution as W
+    n = 8
+    circ = W.adiabatic_circuit(n, 20.0, 0.05)
+    x = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(x, basis=0)
+    st.apply_circuit(circ.gates, fuse=True)
+    st.canonicalize()
+    st.sync()
+    H1 = E.tfim_hamiltonian(n, 1.0)
+    e0 = np.linalg.eigvalsh(H1)[0]
+    assert abs(E.energy(x.cpu().numpy(), H1) - e0) <= 0.02 * abs(e0)
