@@ -61,7 +61,8 @@ typedef enum {
     QJ_ERR_DTYPE = 6,              /* unknown dtype */
     QJ_ERR_CUDA = 7,               /* a CUDA runtime error (launch or asynchronous) */
     QJ_ERR_NCCL = 8,               /* a NCCL error in the multi-GPU layer */
-    QJ_ERR_UNSUPPORTED = 9         /* valid request this build does not implement */
+    QJ_ERR_UNSUPPORTED = 9,        /* valid request this build does not implement */
+    QJ_ERR_ZERO_PROBABILITY = 10   /* collapse / sampling on an outcome set of probability ~0 */
 } qj_status;
 
 typedef enum { QJ_C64 = 0, QJ_C128 = 1 } qj_dtype;
@@ -174,6 +175,74 @@ qj_status qj_state_canonicalize(qj_state s);
  * owned DEVICE memory of the state's real type (float for C64, double for
  * C128).  Sharded states: out_dev must hold the full output. */
 qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev);
+
+/* ---- measurement ("a custom operator for collapsing and
+ * re-normalizing states and a method for sampling shot frequencies based on
+ * Metropolis algorithm"; R26-R28) ---------------------------------
+ *
+ * Outcomes are integers over the listed qubits, first listed = most
+ * significant bit (the qj_probabilities convention).
+ *
+ * qj_collapse: P = sum |psi_i|^2 over the basis states consistent with
+ * `outcome` (fp64, fixed reduction order: deterministic); if P <= 1e-14 the
+ * call fails with QJ_ERR_ZERO_PROBABILITY and the state is untouched;
+ * otherwise consistent amplitudes are divided by sqrt(P) and all others set to
+ * 0, in place.  `prob_out` (host, may be NULL) receives P.
+ * Synchronises the handle's stream once (P is checked on the host).  Works on
+ * remapped, virtual-sharded and NCCL-sharded states (P is all-reduced).
+ * Errors: INVALID_ARG (NULL, nq < 1, outcome >= 2^nq), INDEX_OUT_OF_RANGE,
+ * OVERLAPPING_QUBITS, ZERO_PROBABILITY. */
+qj_status qj_collapse(qj_state s, const int* qubits, int nq, uint64_t outcome, double* prob_out);
+
+typedef enum {
+    QJ_SAMPLE_DIRECT = 0,          /* exact inverse CDF (2^-60 fixed point, R27)      */
+    QJ_SAMPLE_METROPOLIS = 1,      /* Metropolis chains, uniform proposal (R28)       */
+    QJ_SAMPLE_METROPOLIS_FLIP = 2  /* Metropolis chains, single-bit-flip proposal     */
+} qj_sample_method;
+
+#define QJ_AUTO UINT64_MAX
+
+typedef struct {
+    int method;        /* qj_sample_method                                         */
+    uint32_t nchains;  /* Metropolis: independent chains; 0 = min(nshots, 4096)   */
+    uint64_t burnin;   /* Metropolis: steps per chain before recording; QJ_AUTO =
+                          max(100, ceil(ceil(nshots / nchains) / 10))              */
+} qj_sample_opts;
+
+/* Draw `nshots` outcomes from the distribution `probs_dev` (DEVICE, 2^nbits
+ * fp64 weights, need not be normalised; negative / NaN entries count as 0;
+ * sum < 16) with the counter-based generator Philox4x32-10 keyed by `seed`:
+ * shot i of the direct method uses counter (i mod 2^32, i >> 32, 0, 0) (R27), chain c
+ * step t of Metropolis uses counter (t, c, 1, 0) (R28), so results depend only
+ * on (probs, nshots, seed, opts), never on the device or launch shape.
+ * Outputs (DEVICE, each may be NULL, not both): samples_dev[nshots] int64
+ * outcomes (Metropolis: chain c's shots contiguous at offset
+ * c*floor(nshots/C) + min(c, nshots mod C)); counts_dev[2^nbits] uint64
+ * frequencies, ADDED to (zero it first).  opts NULL = direct.  Work is
+ * enqueued on `stream` (cudaStream_t, NULL = legacy default).  The direct
+ * method synchronises once to check the total (ZERO_PROBABILITY if 0) and
+ * allocates its CDF scratch (8 (2^nbits + 2^nbits/4096 + 1) bytes) stream-
+ * ordered.  Errors: INVALID_ARG (nshots == 0, NULL outputs, bad opts),
+ * CAPACITY (nbits > 34, Metropolis burnin + shots per chain >= 2^32 - 1),
+ * ZERO_PROBABILITY. */
+qj_status qj_sample_distribution(const double* probs_dev, int nbits, uint64_t nshots, uint64_t seed,
+                                 const qj_sample_opts* opts, int64_t* samples_dev, uint64_t* counts_dev,
+                                 void* stream);
+
+/* Shots over the marginal of the listed qubits of the state (the fp64 bins
+ * of qj_probabilities, all-reduced across NCCL ranks; nq <= 30), then
+ * qj_sample_distribution on the handle's stream with the handle's scratch.
+ * The state is not modified.  Bins come from fp64 atomics, so their last
+ * bit may differ between runs; a draw can change only when that moves a
+ * decision boundary (probability ~1e-16 per draw). */
+qj_status qj_sample(qj_state s, const int* qubits, int nq, uint64_t nshots, uint64_t seed,
+                    const qj_sample_opts* opts, int64_t* samples_dev, uint64_t* counts_dev);
+
+/* One projective measurement of the listed qubits: draw one outcome with the
+ * direct method (shot 0 of `seed`), then qj_collapse onto it.  `outcome_out`
+ * (host) receives it, `prob_out` (host, may be NULL) its probability. */
+qj_status qj_measure(qj_state s, const int* qubits, int nq, uint64_t seed, uint64_t* outcome_out,
+                     double* prob_out);
 
 /* Block until all work enqueued on the handle has finished; reports
  * asynchronous CUDA errors. */

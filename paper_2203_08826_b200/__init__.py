@@ -5,6 +5,7 @@ amplitude work runs in the in-tree sm_100a library ``lib/libqj.so``.
 """
 
 from .qj import (QJ_C64, QJ_C128, QJ_FUSE, QJ_KEEP, QJError, State, insert_zero_bits,  # noqa: F401
-                 lib)
+                 lib, sample_distribution)
 
-__all__ = ["State", "QJError", "lib", "insert_zero_bits", "QJ_C64", "QJ_C128", "QJ_FUSE", "QJ_KEEP"]
+__all__ = ["State", "QJError", "lib", "insert_zero_bits", "sample_distribution", "QJ_C64", "QJ_C128",
+           "QJ_FUSE", "QJ_KEEP"]

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -58,6 +59,8 @@ struct qj_state_s {
     int rank = 0, nranks = 1;
     void* xbuf = nullptr;  // exchange staging ring
     size_t xbuf_bytes = 0;
+    void* mbuf = nullptr;  // measurement scratch (norm partials, sampler CDF); never in a captured graph
+    size_t mbuf_bytes = 0;
     int total_shards() const { return comm ? nranks : (int)shards.size(); }
     // circuits seen before: plan + prepared tile passes (+ a CUDA graph)
     struct CachedPlan {
@@ -107,6 +110,20 @@ qj_status ensure_scratch(qj_state s, size_t bytes) {
     cudaError_t e = cudaMalloc(&s->scratch, bytes);
     if (e != cudaSuccess) return cuda_fail(e, "scratch alloc");
     s->scratch_bytes = bytes;
+    return QJ_OK;
+}
+
+qj_status ensure_mbuf(qj_state s, size_t bytes) {
+    if (s->mbuf_bytes >= bytes) return QJ_OK;
+    if (s->mbuf) {
+        cudaStreamSynchronize(s->stream);
+        cudaFree(s->mbuf);
+        s->mbuf = nullptr;
+        s->mbuf_bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&s->mbuf, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "measurement scratch alloc");
+    s->mbuf_bytes = bytes;
     return QJ_OK;
 }
 
@@ -673,6 +690,7 @@ qj_status qj_state_free(qj_state s) {
     if (s->scratch) cudaFree(s->scratch);
     if (s->bins) cudaFree(s->bins);
     if (s->xbuf) cudaFree(s->xbuf);
+    if (s->mbuf) cudaFree(s->mbuf);
     delete s;
     return QJ_OK;
 }
@@ -765,40 +783,11 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
     return apply_lgates(s, gs, (flags & QJ_FUSE) != 0);
 }
 
-qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev) {
-    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
-    if (!out_dev) return fail(QJ_ERR_INVALID_ARG, "out_dev is NULL");
+// fp64 marginal over the listed logical qubits into s->bins[2^nq] (all-reduced
+// across NCCL ranks).  Validates the qubit list.
+static qj_status marginal_bins(qj_state s, const int* qubits, int nq) {
     cudaError_t e = cudaSuccess;
     const int n = s->n, nl = s->nl;
-    if (qubits == nullptr && nq == -1) {
-        bool identity = true;
-        for (int q = 0; q < n; ++q) identity &= (s->phys[q] == n - 1 - q);
-        const size_t rb = s->dt == QJ_C64 ? 4 : 8;
-        if (s->comm && !identity)
-            return fail(QJ_ERR_UNSUPPORTED, "full probabilities of a remapped NCCL-sharded state: call qj_state_canonicalize first");
-        for (size_t i = 0; i < s->shards.size(); ++i) {
-            const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
-            if (identity) {
-                // NCCL-sharded: out_dev holds this rank's 2^n_local values
-                void* dst = static_cast<unsigned char*>(out_dev) + (s->comm ? 0 : rb * (r << nl));
-                e = by_dtype(s->dt, [&](auto z) {
-                    using R = decltype(z);
-                    return run_prob_full<R>(s->shards[i], nl, dst, s->stream, s->ls);
-                });
-            } else {
-                int cpos[64];
-                for (int q = 0; q < n; ++q) cpos[s->phys[q]] = n - 1 - q;
-                e = by_dtype(s->dt, [&](auto z) {
-                    using R = decltype(z);
-                    return run_prob_scatter<R>(s->shards[i], nl, r, n, cpos, out_dev, s->stream, s->ls);
-                });
-            }
-            if (e != cudaSuccess) return cuda_fail(e, "probabilities launch");
-        }
-        s->ctr.launches = s->ls.launches;
-        return QJ_OK;
-    }
-    if (!qubits) return fail(QJ_ERR_INVALID_ARG, "qubits is NULL (use nq=-1 for the full vector)");
     if (nq < 1 || nq > n) return fail(QJ_ERR_INVALID_ARG, "nq=%d outside [1,%d]", nq, n);
     if (nq > 30) return fail(QJ_ERR_CAPACITY, "marginal over %d qubits is too large (max 30)", nq);
     uint64_t seen_lo = 0;
@@ -839,6 +828,45 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
                                               static_cast<ncclComm_t>(s->comm), s->stream);
         if (r != ncclSuccess) return fail(QJ_ERR_NCCL, "marginal all-reduce: %s", api->GetErrorString(r));
     }
+    return QJ_OK;
+}
+
+qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (!out_dev) return fail(QJ_ERR_INVALID_ARG, "out_dev is NULL");
+    cudaError_t e = cudaSuccess;
+    const int n = s->n, nl = s->nl;
+    if (qubits == nullptr && nq == -1) {
+        bool identity = true;
+        for (int q = 0; q < n; ++q) identity &= (s->phys[q] == n - 1 - q);
+        const size_t rb = s->dt == QJ_C64 ? 4 : 8;
+        if (s->comm && !identity)
+            return fail(QJ_ERR_UNSUPPORTED, "full probabilities of a remapped NCCL-sharded state: call qj_state_canonicalize first");
+        for (size_t i = 0; i < s->shards.size(); ++i) {
+            const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
+            if (identity) {
+                // NCCL-sharded: out_dev holds this rank's 2^n_local values
+                void* dst = static_cast<unsigned char*>(out_dev) + (s->comm ? 0 : rb * (r << nl));
+                e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return run_prob_full<R>(s->shards[i], nl, dst, s->stream, s->ls);
+                });
+            } else {
+                int cpos[64];
+                for (int q = 0; q < n; ++q) cpos[s->phys[q]] = n - 1 - q;
+                e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return run_prob_scatter<R>(s->shards[i], nl, r, n, cpos, out_dev, s->stream, s->ls);
+                });
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "probabilities launch");
+        }
+        s->ctr.launches = s->ls.launches;
+        return QJ_OK;
+    }
+    if (!qubits) return fail(QJ_ERR_INVALID_ARG, "qubits is NULL (use nq=-1 for the full vector)");
+    if (qj_status st = marginal_bins(s, qubits, nq)) return st;
+    const size_t nb = (size_t)1 << nq;
     e = by_dtype(s->dt, [&](auto z) {
         using R = decltype(z);
         return run_bins_to_out<R>(s->bins, nb, out_dev, s->stream, s->ls);
@@ -846,6 +874,176 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
     if (e != cudaSuccess) return cuda_fail(e, "bins launch");
     s->ctr.launches = s->ls.launches;
     return QJ_OK;
+}
+
+// ------------------------------------------------------------------ measurement
+static qj_status check_qubit_list(qj_state s, const int* qubits, int nq) {
+    if (!qubits) return fail(QJ_ERR_INVALID_ARG, "qubits is NULL");
+    if (nq < 1 || nq > s->n) return fail(QJ_ERR_INVALID_ARG, "nq=%d outside [1,%d]", nq, s->n);
+    uint64_t seen = 0;
+    for (int i = 0; i < nq; ++i) {
+        const int q = qubits[i];
+        if (q < 0 || q >= s->n) return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "qubit %d out of range [0,%d)", q, s->n);
+        if (seen & (1ull << q)) return fail(QJ_ERR_OVERLAPPING_QUBITS, "qubit %d listed twice", q);
+        seen |= 1ull << q;
+    }
+    return QJ_OK;
+}
+
+qj_status qj_collapse(qj_state s, const int* qubits, int nq, uint64_t outcome, double* prob_out) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (qj_status st = check_qubit_list(s, qubits, nq)) return st;
+    if (nq < 64 && (outcome >> nq) != 0)
+        return fail(QJ_ERR_INVALID_ARG, "outcome %llu >= 2^%d", (unsigned long long)outcome, nq);
+    const int nl = s->nl;
+    int pos[64], val[64], m = 0;
+    uint64_t gmask = 0, gwant = 0, mask = 0, want = 0;
+    for (int i = 0; i < nq; ++i) {
+        const int b = s->phys[qubits[i]];
+        const int v = (int)((outcome >> (nq - 1 - i)) & 1u);
+        if (b < nl) {
+            pos[m] = b;
+            val[m++] = v;
+            mask |= 1ull << b;
+            if (v) want |= 1ull << b;
+        } else {
+            gmask |= 1ull << (b - nl);
+            if (v) gwant |= 1ull << (b - nl);
+        }
+    }
+    const size_t nsh = s->shards.size();
+    const size_t kPartials = 2048;
+    if (qj_status st = ensure_mbuf(s, (kPartials + nsh) * sizeof(double))) return st;
+    double* partial = static_cast<double*>(s->mbuf);
+    double* outs = partial + kPartials;
+    cudaError_t e = cudaSuccess;
+    std::vector<char> match(nsh);
+    for (size_t i = 0; i < nsh; ++i) {
+        const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
+        match[i] = (r & gmask) == gwant;
+        if (match[i]) {
+            e = by_dtype(s->dt, [&](auto z) {
+                using R = decltype(z);
+                return run_subspace_norm<R>(s->shards[i], nl, pos, val, m, partial, outs + i, s->stream, s->ls);
+            });
+        } else {
+            e = cudaMemsetAsync(outs + i, 0, sizeof(double), s->stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "collapse norm");
+    }
+    if (s->comm) {
+        const char* why = nullptr;
+        const NcclApi* api = nccl_api(&why);
+        if (!api) return fail(QJ_ERR_NCCL, "NCCL unavailable: %s", why ? why : "?");
+        const ncclResult_t r = api->AllReduce(outs, outs, 1, ncclFloat64, ncclSum, static_cast<ncclComm_t>(s->comm),
+                                              s->stream);
+        if (r != ncclSuccess) return fail(QJ_ERR_NCCL, "collapse all-reduce: %s", api->GetErrorString(r));
+    }
+    std::vector<double> h(nsh);
+    e = cudaMemcpyAsync(h.data(), outs, nsh * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "collapse norm readback");
+    double P = 0.0;
+    for (size_t i = 0; i < nsh; ++i) P += h[i];  // shard order: deterministic
+    if (prob_out) *prob_out = P;
+    if (!(P > 1e-14)) return fail(QJ_ERR_ZERO_PROBABILITY, "P(outcome=%llu) = %.3e <= 1e-14", (unsigned long long)outcome, P);
+    const double scale = 1.0 / std::sqrt(P);
+    const size_t bytes = ((size_t)s->amp_bytes) << nl;
+    for (size_t i = 0; i < nsh; ++i) {
+        if (match[i]) {
+            e = by_dtype(s->dt, [&](auto z) {
+                using R = decltype(z);
+                return run_collapse_apply<R>(s->shards[i], nl, mask, want, scale, s->stream, s->ls);
+            });
+        } else {
+            e = cudaMemsetAsync(s->shards[i], 0, bytes, s->stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "collapse apply");
+    }
+    s->ctr.launches = s->ls.launches;
+    return QJ_OK;
+}
+
+static qj_status sample_impl(const double* p, int nbits, uint64_t nshots, uint64_t seed, const qj_sample_opts* opts,
+                             int64_t* samples, uint64_t* counts, cudaStream_t st, void* scratch, LaunchStats& ls) {
+    if (!p) return fail(QJ_ERR_INVALID_ARG, "probabilities are NULL");
+    if (nbits < 0 || nbits > 34) return fail(QJ_ERR_CAPACITY, "nbits=%d outside [0,34]", nbits);
+    if (nshots == 0) return fail(QJ_ERR_INVALID_ARG, "nshots must be >= 1");
+    if (!samples && !counts) return fail(QJ_ERR_INVALID_ARG, "samples and counts are both NULL");
+    const int method = opts ? opts->method : QJ_SAMPLE_DIRECT;
+    const uint64_t nb = 1ull << nbits;
+    cudaError_t e = cudaSuccess;
+    if (method == QJ_SAMPLE_DIRECT) {
+        void* buf = scratch;
+        if (!buf) {
+            e = cudaMallocAsync(&buf, direct_scratch_bytes(nb), st);
+            if (e != cudaSuccess) return cuda_fail(e, "sampler scratch alloc");
+        }
+        e = run_direct_cdf(p, nb, buf, st, ls);
+        uint64_t total = 0;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&total, direct_total_ptr(buf, nb), sizeof(total), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess && total != 0) e = run_direct_shots(buf, nb, nshots, seed, samples, counts, st, ls);
+        if (!scratch) cudaFreeAsync(buf, st);
+        if (e != cudaSuccess) return cuda_fail(e, "direct sampler");
+        if (total == 0) return fail(QJ_ERR_ZERO_PROBABILITY, "all %llu probabilities are zero", (unsigned long long)nb);
+        return QJ_OK;
+    }
+    if (method != QJ_SAMPLE_METROPOLIS && method != QJ_SAMPLE_METROPOLIS_FLIP)
+        return fail(QJ_ERR_INVALID_ARG, "unknown sampling method %d", method);
+    uint64_t C = opts->nchains ? opts->nchains : std::min<uint64_t>(nshots, 4096);
+    const uint64_t per = (nshots + C - 1) / C;
+    const uint64_t B = opts->burnin == QJ_AUTO ? std::max<uint64_t>(100, (per + 9) / 10) : opts->burnin;
+    if (B >= 0xFFFFFFFFull || per >= 0xFFFFFFFFull - B)
+        return fail(QJ_ERR_CAPACITY, "burn-in %llu + %llu shots per chain exceed the 2^32 - 1 step counter",
+                    (unsigned long long)B, (unsigned long long)per);
+    e = run_metropolis(p, nbits, nshots, seed, (uint32_t)C, B, method == QJ_SAMPLE_METROPOLIS_FLIP, samples, counts,
+                       st, ls);
+    if (e != cudaSuccess) return cuda_fail(e, "Metropolis sampler");
+    return QJ_OK;
+}
+
+qj_status qj_sample_distribution(const double* probs_dev, int nbits, uint64_t nshots, uint64_t seed,
+                                 const qj_sample_opts* opts, int64_t* samples_dev, uint64_t* counts_dev,
+                                 void* stream) {
+    LaunchStats ls;
+    return sample_impl(probs_dev, nbits, nshots, seed, opts, samples_dev, counts_dev,
+                       static_cast<cudaStream_t>(stream), nullptr, ls);
+}
+
+qj_status qj_sample(qj_state s, const int* qubits, int nq, uint64_t nshots, uint64_t seed,
+                    const qj_sample_opts* opts, int64_t* samples_dev, uint64_t* counts_dev) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (qj_status st = check_qubit_list(s, qubits, nq)) return st;
+    if (nshots == 0) return fail(QJ_ERR_INVALID_ARG, "nshots must be >= 1");
+    if (!samples_dev && !counts_dev) return fail(QJ_ERR_INVALID_ARG, "samples and counts are both NULL");
+    if (qj_status st = marginal_bins(s, qubits, nq)) return st;
+    const bool direct = !opts || opts->method == QJ_SAMPLE_DIRECT;
+    void* scratch = nullptr;
+    if (direct) {
+        if (qj_status st = ensure_mbuf(s, direct_scratch_bytes(1ull << nq))) return st;
+        scratch = s->mbuf;
+    }
+    qj_status st = sample_impl(s->bins, nq, nshots, seed, opts, samples_dev, counts_dev, s->stream, scratch, s->ls);
+    s->ctr.launches = s->ls.launches;
+    return st;
+}
+
+qj_status qj_measure(qj_state s, const int* qubits, int nq, uint64_t seed, uint64_t* outcome_out, double* prob_out) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (!outcome_out) return fail(QJ_ERR_INVALID_ARG, "outcome_out is NULL");
+    if (qj_status st = check_qubit_list(s, qubits, nq)) return st;
+    if (qj_status st = marginal_bins(s, qubits, nq)) return st;
+    const size_t sb = direct_scratch_bytes(1ull << nq);
+    if (qj_status st = ensure_mbuf(s, sb + 64)) return st;
+    int64_t* shot = reinterpret_cast<int64_t*>(static_cast<char*>(s->mbuf) + ((sb + 15) & ~size_t(15)));
+    if (qj_status st = sample_impl(s->bins, nq, 1, seed, nullptr, shot, nullptr, s->stream, s->mbuf, s->ls)) return st;
+    int64_t h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, shot, sizeof(h), cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "measurement readback");
+    *outcome_out = (uint64_t)h;
+    return qj_collapse(s, qubits, nq, (uint64_t)h, prob_out);
 }
 
 qj_status qj_fuse_circuit(int n, const qj_gate* in, int nin, int max_qubits, qj_gate* out, double* mats, int max_out,

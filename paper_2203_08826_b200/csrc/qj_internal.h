@@ -69,4 +69,19 @@ cudaError_t run_prob_scatter(const void* psi, int nl, uint64_t shard, int n, con
 template <typename R>
 cudaError_t run_exchange(void* a, void* b, int nl, int L, cudaStream_t st, LaunchStats& ls);
 
+// measurement (measure.cu): consistent-subspace norm (fp64, deterministic
+// order: partial[kNormBlocks] then *out), collapse write pass, samplers.
+template <typename R>
+cudaError_t run_subspace_norm(const void* psi, int nl, const int* pos, const int* val, int m, double* partial,
+                              double* out, cudaStream_t st, LaunchStats& ls);
+template <typename R>
+cudaError_t run_collapse_apply(void* psi, int nl, uint64_t mask, uint64_t want, double scale, cudaStream_t st,
+                               LaunchStats& ls);
+size_t direct_scratch_bytes(uint64_t nbins);
+cudaError_t run_direct_cdf(const double* p, uint64_t nbins, void* scratch, cudaStream_t st, LaunchStats& ls);
+const uint64_t* direct_total_ptr(const void* scratch, uint64_t nbins);
+cudaError_t run_direct_shots(const void* scratch, uint64_t nbins, uint64_t nshots, uint64_t seed, int64_t* samples,
+                             uint64_t* counts, cudaStream_t st, LaunchStats& ls);
+cudaError_t run_metropolis(const double* p, int m, uint64_t nshots, uint64_t seed, uint32_t nchains, uint64_t burnin,
+                           bool flip, int64_t* samples, uint64_t* counts, cudaStream_t st, LaunchStats& ls);
 }  // namespace qj

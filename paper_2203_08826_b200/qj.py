@@ -24,14 +24,19 @@ MAX_TARGETS, MAX_CONTROLS = 8, 16
 KIND = {"dense": 0, "x": 1, "z": 2, "swap": 3, "fsim": 4, "diag": 5}
 STATUS = {0: "QJ_OK", 1: "QJ_ERR_INVALID_ARG", 2: "QJ_ERR_INDEX_OUT_OF_RANGE",
           3: "QJ_ERR_OVERLAPPING_QUBITS", 4: "QJ_ERR_TOO_MANY_TARGETS", 5: "QJ_ERR_CAPACITY",
-          6: "QJ_ERR_DTYPE", 7: "QJ_ERR_CUDA", 8: "QJ_ERR_NCCL", 9: "QJ_ERR_UNSUPPORTED"}
+          6: "QJ_ERR_DTYPE", 7: "QJ_ERR_CUDA", 8: "QJ_ERR_NCCL", 9: "QJ_ERR_UNSUPPORTED",
+          10: "QJ_ERR_ZERO_PROBABILITY"}
+
+SAMPLE_METHODS = {"direct": 0, "metropolis": 1, "metropolis_flip": 2}
+AUTO = (1 << 64) - 1
 
 EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state_free",
            "qj_apply_gate", "qj_apply_x", "qj_apply_z", "qj_apply_swap", "qj_apply_fsim",
            "qj_apply_diagonal", "qj_apply_circuit", "qj_probabilities", "qj_sync",
            "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
            "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
-           "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit"]
+           "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit", "qj_collapse",
+           "qj_sample_distribution", "qj_sample", "qj_measure"]
 
 
 class QJError(RuntimeError):
@@ -56,6 +61,16 @@ class qj_counters(ctypes.Structure):
 class qj_profile_entry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64),
                 ("total_ms", ctypes.c_double), ("alg_bytes", ctypes.c_double)]
+
+
+class qj_sample_opts(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int), ("nchains", ctypes.c_uint32), ("burnin", ctypes.c_uint64)]
+
+
+def sample_opts(method="direct", nchains=0, burnin=None):
+    if method not in SAMPLE_METHODS:
+        raise ValueError(f"unknown sampling method {method!r} (one of {sorted(SAMPLE_METHODS)})")
+    return qj_sample_opts(SAMPLE_METHODS[method], int(nchains), AUTO if burnin is None else int(burnin))
 
 
 class qj_plan_step(ctypes.Structure):
@@ -106,6 +121,10 @@ def lib():
         "qj_exchange_peer": ([I, I, IP, IP], None),
         "qj_fuse_circuit": ([I, ctypes.POINTER(qj_gate), I, I, ctypes.POINTER(qj_gate), ctypes.POINTER(ctypes.c_double),
                              I, IP, IP], S),
+        "qj_collapse": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_double)], S),
+        "qj_sample_distribution": ([P, I, U64, U64, ctypes.POINTER(qj_sample_opts), P, P, P], S),
+        "qj_sample": ([P, IP, I, U64, U64, ctypes.POINTER(qj_sample_opts), P, P], S),
+        "qj_measure": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double)], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -123,6 +142,35 @@ def _check(code: int):
 def _ints(xs):
     xs = [int(x) for x in (xs or ())]
     return (ctypes.c_int * max(1, len(xs)))(*xs), len(xs)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def sample_distribution(probs, nshots, seed, method="direct", nchains=0, burnin=None,
+                        samples=True, counts=True, stream=None):
+    """Shots from a fp64 device tensor of 2^m weights (qj_sample_distribution)
+    on `stream` (default: torch's current stream).  Returns (samples, counts)."""
+    import torch
+
+    if probs.dtype != torch.float64 or not probs.is_cuda or not probs.is_contiguous():
+        raise ValueError("probs must be a contiguous float64 CUDA tensor")
+    nb = probs.numel()
+    m = nb.bit_length() - 1
+    if nb != 1 << m:
+        raise ValueError("len(probs) must be a power of two")
+    stream = stream or torch.cuda.current_stream(probs.device)
+    opts = sample_opts(method, nchains, burnin)
+    smp = torch.empty(int(nshots), dtype=torch.int64, device=probs.device) if samples else None
+    cnt = None
+    if counts:
+        with torch.cuda.stream(stream):
+            cnt = torch.zeros(nb, dtype=torch.int64, device=probs.device)
+    _check(lib().qj_sample_distribution(ctypes.c_void_p(probs.data_ptr()), m, ctypes.c_uint64(int(nshots)),
+                                        ctypes.c_uint64(int(seed)), ctypes.byref(opts), _ptr(smp), _ptr(cnt),
+                                        ctypes.c_void_p(stream.cuda_stream)))
+    return smp, cnt
 
 
 def insert_zero_bits(g: int, sorted_positions) -> int:
@@ -386,6 +434,41 @@ class State:
             out = torch.empty(size, dtype=self.real_dtype, device=self.device)
         _check(lib().qj_probabilities(self._h, q, nq, ctypes.c_void_p(out.data_ptr())))
         return out
+
+    # ---- measurement (R26-R28)
+    def collapse(self, qubits, outcome):
+        """Project onto `outcome` of the listed qubits (first = MSB) and
+        renormalise in place; returns P(outcome).  Raises QJError
+        (QJ_ERR_ZERO_PROBABILITY) if P <= 1e-14, leaving the state untouched."""
+        q, nq = _ints(qubits)
+        p = ctypes.c_double()
+        _check(lib().qj_collapse(self._h, q, nq, ctypes.c_uint64(int(outcome)), ctypes.byref(p)))
+        return p.value
+
+    def sample(self, qubits, nshots, seed, method="direct", nchains=0, burnin=None,
+               samples=True, counts=True):
+        """Shots over the marginal of `qubits`: returns (samples int64[nshots] or
+        None, counts int64[2^nq] or None), device tensors on the handle's stream."""
+        import torch
+
+        q, nq = _ints(qubits)
+        opts = sample_opts(method, nchains, burnin)
+        smp = torch.empty(int(nshots), dtype=torch.int64, device=self.device) if samples else None
+        cnt = None
+        if counts:
+            with torch.cuda.stream(self.stream):
+                cnt = torch.zeros(1 << nq, dtype=torch.int64, device=self.device)
+        _check(lib().qj_sample(self._h, q, nq, ctypes.c_uint64(int(nshots)), ctypes.c_uint64(int(seed)),
+                               ctypes.byref(opts), _ptr(smp), _ptr(cnt)))
+        return smp, cnt
+
+    def measure(self, qubits, seed):
+        """Draw one outcome of `qubits` (direct method) and collapse onto it:
+        returns (outcome, probability)."""
+        q, nq = _ints(qubits)
+        o, p = ctypes.c_uint64(), ctypes.c_double()
+        _check(lib().qj_measure(self._h, q, nq, ctypes.c_uint64(int(seed)), ctypes.byref(o), ctypes.byref(p)))
+        return int(o.value), p.value
 
     def counters(self, reset=False):
         c = qj_counters()

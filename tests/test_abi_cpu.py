@@ -178,3 +178,37 @@ def test_no_cpu_fallback_without_gpu():
     h = fake_state(6)
     assert L.qj_apply_x(h, 0, None, 0) == 7
     assert b"cuda" in L.qj_last_error().lower() or b"CUDA" in L.qj_last_error()
+
+
+def test_measurement_validation_codes():
+    """qj_collapse / qj_sample / qj_measure / qj_sample_distribution reject bad
+    arguments before any CUDA call (include/qj.h measurement section)."""
+    L = Q.lib()
+    h = fake_state(6)
+    p = ctypes.c_double()
+    U = ctypes.c_uint64
+    assert L.qj_collapse(None, ints([0]), 1, U(0), ctypes.byref(p)) == 1
+    assert L.qj_collapse(h, None, 1, U(0), None) == 1
+    assert L.qj_collapse(h, ints([0]), 0, U(0), None) == 1
+    assert L.qj_collapse(h, ints([0, 1]), 2, U(4), None) == 1
+    assert L.qj_collapse(h, ints([6]), 1, U(0), None) == 2
+    assert L.qj_collapse(h, ints([2, 2]), 2, U(0), None) == 3
+    opts = Q.sample_opts("metropolis")
+    dev = ctypes.c_void_p(0x20000)
+    assert L.qj_sample(h, ints([0]), 1, U(0), U(1), ctypes.byref(opts), dev, None) == 1
+    assert L.qj_sample(h, ints([0]), 1, U(5), U(1), ctypes.byref(opts), None, None) == 1
+    assert L.qj_sample(h, ints([9]), 1, U(5), U(1), ctypes.byref(opts), dev, None) == 2
+    o = ctypes.c_uint64()
+    assert L.qj_measure(h, ints([0]), 1, U(1), None, None) == 1
+    assert L.qj_measure(h, ints([1, 1]), 2, U(1), ctypes.byref(o), None) == 3
+    assert L.qj_sample_distribution(None, 3, U(5), U(1), None, dev, None, None) == 1
+    assert L.qj_sample_distribution(dev, 35, U(5), U(1), None, dev, None, None) == 5
+    assert L.qj_sample_distribution(dev, 3, U(0), U(1), None, dev, None, None) == 1
+    assert L.qj_sample_distribution(dev, 3, U(5), U(1), None, None, None, None) == 1
+    bad = Q.qj_sample_opts(7, 0, Q.AUTO)
+    assert L.qj_sample_distribution(dev, 3, U(5), U(1), ctypes.byref(bad), dev, None, None) == 1
+    long_chain = Q.sample_opts("metropolis", nchains=1, burnin=2**32)
+    assert L.qj_sample_distribution(dev, 3, U(5), U(1), ctypes.byref(long_chain), dev, None, None) == 5
+    with pytest.raises(ValueError):
+        Q.sample_opts("gibbs")
+    assert L.qj_state_free(h) == 0
