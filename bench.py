@@ -129,6 +129,13 @@ def make_workload(name):
         return dict(n=20, dtype="c64", circ=C.variational(20, layers=20), basis=0, readout=list(range(10)))
     if name == "sup32_c64":
         return dict(n=32, dtype="c64", circ=C.supremacy(4, 8, 20), basis=0, readout=list(range(10)))
+    if name in ("tfim10_c128", "tfim20_c128"):
+        # adiabatic TFIM evolution on 10 / 20 qubits by Trotter
+        # decomposition; T = 1, dt = 0.01 (100 second-order steps, R24)
+        from workloads import evolution as E
+        nq = 10 if name.startswith("tfim10") else 20
+        return dict(n=nq, dtype="c128", circ=E.adiabatic_circuit(nq, 1.0, 0.01), basis=0,
+                    readout=list(range(10)))
     if name == "qft10_c128":
         return dict(n=10, dtype="c128", circ=C.qft(10), basis=SEED_X & 1023, readout=list(range(10)))
     raise SystemExit(f"unknown workload {name}")
@@ -189,12 +196,47 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------- qj arm
+L2_FLUSH_BELOW = 256 << 20  # states smaller than 2x the 126 MB L2 are timed with a flush between steps
+
+
+def needs_flush(wl):
+    return ((16 if wl["dtype"] == "c128" else 8) << wl["n"]) < L2_FLUSH_BELOW
+
+
+def timed_steps(torch, stream, steps, step, flush_buf):
+    """Device time (ms) of `steps` calls of step() on `stream`.  Without a
+    flush buffer: one event pair around all steps (the state is larger than
+    L2).  With one: every step is preceded by a 256 MiB write of the flush
+    buffer (outside the events) and timed by its own event pair; the sum is
+    returned."""
+    if flush_buf is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        stream.synchronize()
+        return e0.elapsed_time(e1)
+    pairs = []
+    for i in range(steps):
+        with torch.cuda.stream(stream):
+            flush_buf.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        pairs.append((a, b))
+    stream.synchronize()
+    return sum(a.elapsed_time(b) for a, b in pairs)
+
+
 def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_gates=False):
     """Time `steps` steps (state reset + circuit + 10-qubit marginal) on the
     device with CUDA events; returns timings, per-kind profile and counters."""
     n = wl["n"]
     tdt = torch.complex128 if wl["dtype"] == "c128" else torch.complex64
     stream = torch.cuda.Stream(dev)
+    flush_buf = torch.empty(L2_FLUSH_BELOW, dtype=torch.uint8, device=dev) if needs_flush(wl) else None
     psi = torch.empty(1 << n, dtype=tdt, device=dev)
     st = qj.State(psi, basis=None, stream=stream)
     packed = st.pack_circuit(wl["circ"].gates)
@@ -221,16 +263,11 @@ def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_g
         step()
     barrier()
     st.counters(reset=True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     with ClockSampler(dev.index) as clk:
-        e0.record(stream)
-        for _ in range(steps):
-            step()
-        e1.record(stream)
+        ms = timed_steps(torch, stream, steps, step, flush_buf)
         torch.cuda.synchronize(dev)
     barrier()
-    ms = e0.elapsed_time(e1)
     ctr = st.counters(reset=True)
     # per-pass device times: a profiled repeat of the same timed steps (CUDA
     # events around every pass on the state's stream; no graph replay)
@@ -238,13 +275,7 @@ def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_g
     if profile:
         st.set_profiling(True)
         st.profile(reset=True)
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        for _ in range(steps):
-            step()
-        p1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms_prof = p0.elapsed_time(p1)
+        ms_prof = timed_steps(torch, stream, steps, step, flush_buf)
         prof = st.profile(reset=True)
         st.set_profiling(False)
         st.counters(reset=True)
@@ -254,7 +285,7 @@ def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_g
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_max = float(t.item())
     return dict(st=st, psi=psi, stream=stream, pbuf=pbuf, ms=ms, ms_max=ms_max, prof=prof, ctr=ctr,
-                clk=clk, dry=dry, ms_prof=ms_prof)
+                clk=clk, dry=dry, ms_prof=ms_prof, flush_buf=flush_buf)
 
 
 def roofline_of(prof, ms_step_total, peak, peak_src, traffic, traffic_src):
@@ -366,18 +397,17 @@ def run_qj(args, rank, world):
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(steps):
+
+    def e2e_step():
         st.reset(wl["basis"])
         st.apply_circuit(gates, fuse=args.fuse)           # packs the host gate list each step
         p = st.probabilities(readout, out=m["pbuf"])
         with torch.cuda.stream(stream):
             host_out.copy_(p, non_blocking=True)
         stream.synchronize()
-    f1.record(stream)
+
+    e2e_ms = timed_steps(torch, stream, steps, e2e_step, m["flush_buf"])
     torch.cuda.synchronize(dev)
-    e2e_ms = f0.elapsed_time(f1)
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -446,8 +476,9 @@ def run_qj(args, rank, world):
                    "basis": wl["basis"], "fuse": bool(args.fuse),
                    "step": "state_reset + apply_circuit + 10-qubit marginal probabilities",
                    "l2": (f"state {state_bytes >> 20} MiB >> 126 MB L2: inputs larger than L2, no flush"
-                          if state_bytes > (256 << 20) else
-                          f"state {state_bytes >> 20} MiB is L2-resident (no flush; latency/L2-bound regime)"),
+                          if not needs_flush(wl) else
+                          f"state {state_bytes >> 20} MiB fits L2: 256 MiB L2 flush before every timed step "
+                          "(outside its CUDA-event pair; per-step event pairs summed)"),
                    "parallelism": f"{world} independent replicas (weak scaling)" if world > 1 else "1 GPU"},
         "effective_gbs": per_step_bytes / (ms_max / steps / 1e3) / 1e9,
         "effective_frac": per_step_bytes / (ms_max / steps / 1e3) / 1e9 / peak,
