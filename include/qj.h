@@ -292,11 +292,11 @@ const char* qj_version(void);
  * local bit positions, and EXCHANGE steps (global bit `gbit` <-> local bit
  * `lbit`).  Gate data are read as complex128.  `phys` (n ints, may be NULL)
  * receives the final logical->physical bit map.  Fused (TILE) steps are
- * reported with type 2 and no payload.  Errors: INVALID_ARG / INDEX / OVERLAP
+ * reported with type 2 and no payload; with QJ_FUSE on one shard of n <= 13 (c128) / 14 (c64) qubits, runs of gates are reported as type 3 (one whole-state shared-memory program, no payload).  Errors: INVALID_ARG / INDEX / OVERLAP
  * as qj_apply_circuit, CAPACITY if more than max_steps steps, UNSUPPORTED for
  * dense payloads larger than 4 targets. */
 typedef struct {
-    int type;                   /* 0 = pass, 1 = exchange, 2 = fused tile pass   */
+    int type;                   /* 0 = pass, 1 = exchange, 2 = tile, 3 = small */
     int shard;                  /* global shard index the pass runs on            */
     int kind;                   /* 0 dense, 1 x, 2 swap, 3 diag, 4 phase, 5 neg    */
     int k;                      /* number of targets                              */

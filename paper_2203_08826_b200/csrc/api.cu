@@ -18,6 +18,7 @@
 #include "planner.h"
 #include "common.cuh"
 #include "dist.h"
+#include "small.h"
 
 using namespace qj;
 
@@ -68,6 +69,7 @@ struct qj_state_s {
         std::vector<Step> steps;
         std::vector<int> phys_after;
         std::vector<PreparedTile> tiles;  // one per TILE step, in order
+        std::vector<PreparedSmall> smalls;  // one per SMALL step, in order
         cudaGraphExec_t exec = nullptr;
         bool graphable = true;
         uint64_t uses = 0, kernels = 0;
@@ -85,9 +87,9 @@ struct qj_state_s {
     std::vector<cudaEvent_t> pool;
 };
 
-static const char* kProfNames[] = {"gate_dense", "gate_x",     "gate_swap", "diag_table",
-                                   "diag_phase", "diag_neg",   "tile",      "exchange"};
-enum { PROF_TILE = 6, PROF_EXCHANGE = 7, PROF_N = 8 };
+static const char* kProfNames[] = {"gate_dense", "gate_x",     "gate_swap", "diag_table", "diag_phase",
+                                   "diag_neg",   "tile",       "exchange",  "small"};
+enum { PROF_TILE = 6, PROF_EXCHANGE = 7, PROF_SMALL = 8, PROF_N = 9 };
 
 namespace {
 
@@ -243,6 +245,12 @@ struct ProfScope {
     }
 };
 
+int prof_kind(const Step& st) {
+    if (st.type == Step::TILE) return PROF_TILE;
+    if (st.type == Step::SMALL) return PROF_SMALL;
+    return st.pass.kind;
+}
+
 // Execute planned steps on the device.
 // Exchange over NCCL (dist.h): this rank trades the half of its shard whose
 // local bit L equals spec.half_bit with the partner, chunk by chunk through
@@ -341,10 +349,11 @@ qj_status execute(qj_state s, const std::vector<Step>& steps) {
         }
         void* ptr = shard_ptr(s, st.shard);
         if (!ptr) continue;  // another rank's shard
-        ProfScope prof(s, st.type == Step::TILE ? PROF_TILE : st.pass.kind, st.alg_bytes);
+        ProfScope prof(s, prof_kind(st), st.alg_bytes);
         e = by_dtype(s->dt, [&](auto z) {
             using R = decltype(z);
             if (st.type == Step::TILE) return run_tile<R>(st.tile, ptr, s->nl, s->stream, s->stg, s->ls);
+            if (st.type == Step::SMALL) return run_small<R>(st.prog, ptr, s->nl, s->stream, s->ls);
             return run_pass<R>(st.pass, ptr, s->nl, s->stream, s->scratch, s->scratch_bytes, s->ls);
         });
         if (e != cudaSuccess) return cuda_fail(e, "pass launch");
@@ -401,12 +410,13 @@ std::vector<uint64_t> plan_key(qj_state s, const qj_gate* gates, int ngates, uin
 void release_plan(qj_state_s::CachedPlan* p) {
     if (p->exec) cudaGraphExecDestroy(p->exec);
     for (auto& t : p->tiles) tile_release(t);
+    for (auto& t : p->smalls) small_release(t);
     delete p;
 }
 
 qj_status run_cached(qj_state s, qj_state_s::CachedPlan& p) {
     cudaError_t e = cudaSuccess;
-    size_t ti = 0;
+    size_t ti = 0, si = 0;
     for (const Step& st : p.steps) {
         if (st.type == Step::EXCHANGE) {
             for (size_t r = 0; r < s->shards.size(); ++r) {
@@ -420,9 +430,11 @@ qj_status run_cached(qj_state s, qj_state_s::CachedPlan& p) {
             }
             continue;
         }
-        ProfScope prof(s, st.type == Step::TILE ? PROF_TILE : st.pass.kind, st.alg_bytes);
+        ProfScope prof(s, prof_kind(st), st.alg_bytes);
         if (st.type == Step::TILE) {
             e = tile_launch_prepared(p.tiles[ti++], s->stream, s->ls);
+        } else if (st.type == Step::SMALL) {
+            e = small_launch(p.smalls[si++], s->stream, s->ls);
         } else {
             void* ptr = shard_ptr(s, st.shard);
             e = by_dtype(s->dt, [&](auto z) {
@@ -508,6 +520,18 @@ qj_status apply_circuit_cached(qj_state s, const qj_gate* gates, int ngates, uin
                 return cuda_fail(e, "tile prepare");
             }
             p->tiles.push_back(std::move(t));
+        } else if (st.type == Step::SMALL) {
+            PreparedSmall t;
+            cudaError_t e = by_dtype(s->dt, [&](auto z) {
+                using R = decltype(z);
+                return small_prepare<R>(st.prog, shard_ptr(s, st.shard), s->nl, t);
+            });
+            if (e != cudaSuccess) {
+                small_release(t);
+                release_plan(p);
+                return cuda_fail(e, "small prepare");
+            }
+            p->smalls.push_back(t);
         } else if (st.type == Step::PASS && st.pass.k > 5 && st.pass.kind == PK_DENSE) {
             p->graphable = false;  // big-k passes stage their matrix with a host copy
             const size_t need = (size_t)s->amp_bytes * ((size_t)1 << (2 * st.pass.k));

@@ -1,5 +1,8 @@
 // planner.cpp -- see planner.h.
 #include "planner.h"
+#include "small.h"
+
+#include <cstdlib>
 
 #include <algorithm>
 #include <cmath>
@@ -178,7 +181,45 @@ void Planner::plan_gate(const PlanContext& ctx, const LGate& g, std::vector<Step
     }
 }
 
+// States that fit one SM's shared memory run whole runs of gates in ONE
+// launch of the SMEM kernel (small.h); passes it does not take (dense k > 4)
+// run as ordinary passes in between.
+static bool small_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("QJ_SMALL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void Planner::plan(const PlanContext& ctx, const std::vector<LGate>& gates, bool fuse, std::vector<Step>& out) {
+    if (fuse && ctx.nshards == 1 && ctx.n <= small_max_qubits(ctx.amp_bytes) && small_enabled()) {
+        std::vector<Step> tmp;
+        Step cur;
+        cur.type = Step::SMALL;
+        const double bytes = 2.0 * ctx.amp_bytes * (double)(1ull << ctx.nl);
+        auto flush = [&]() {
+            if (cur.prog.empty()) return;
+            cur.alg_bytes = bytes;
+            out.push_back(std::move(cur));
+            cur = Step();
+            cur.type = Step::SMALL;
+        };
+        for (const LGate& g : gates) {
+            tmp.clear();
+            plan_gate(ctx, g, tmp);
+            for (Step& st : tmp) {
+                if (st.type == Step::PASS && small_supports(st.pass)) {
+                    cur.prog.push_back(std::move(st.pass));
+                } else {
+                    flush();
+                    out.push_back(std::move(st));
+                }
+            }
+        }
+        flush();
+        return;
+    }
     if (fuse) {
         plan_fused(ctx, gates, out);
         return;

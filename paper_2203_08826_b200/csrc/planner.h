@@ -30,10 +30,11 @@ struct LGate {
 };
 
 struct Step {
-    enum Type { PASS = 0, EXCHANGE = 1, TILE = 2 } type = PASS;
+    enum Type { PASS = 0, EXCHANGE = 1, TILE = 2, SMALL = 3 } type = PASS;
     int shard = 0;
     Pass pass;
     TileSpec tile;
+    std::vector<Pass> prog;  // SMALL: the passes the whole-state SMEM kernel runs (small.h)
     int gbit = 0, lbit = 0;  // EXCHANGE: global bit index j (physical nl + j), local bit L
     double alg_bytes = 0;
 };

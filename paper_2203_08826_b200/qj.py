@@ -185,37 +185,63 @@ def exchange_peer(rank: int, gbit: int):
     return p.value, h.value
 
 
+_GATE_NP = np.dtype({"names": ["kind", "nt", "nc", "targets", "controls", "data"],
+                     "formats": ["<i4", "<i4", "<i4", ("<i4", (MAX_TARGETS,)), ("<i4", (MAX_CONTROLS,)), "<u8"],
+                     "offsets": [0, 4, 8, 12, 44, 112], "itemsize": 120})
+
+
 def pack_gates(gates, np_dtype=np.complex128):
-    """Marshal gate records (kind/targets/controls/data) into a qj_gate array."""
+    """Marshal gate records (kind/targets/controls/data) into a qj_gate array:
+    one numpy record array with the C struct's layout and one contiguous
+    coefficient buffer in the state's dtype.  Returns (qj_gate*, n, keepalive)."""
+    assert ctypes.sizeof(qj_gate) == _GATE_NP.itemsize
     gates = list(gates)
-    arr = (qj_gate * max(1, len(gates)))()
-    keep = []
+    ng = len(gates)
+    rec = np.zeros(max(1, ng), dtype=_GATE_NP)
+    kinds = [0] * ng
+    nts = [0] * ng
+    ncs = [0] * ng
+    tg = [0] * (MAX_TARGETS * max(1, ng))
+    ct = [0] * (MAX_CONTROLS * max(1, ng))
+    parts, owner, lens = [], [], []
+    ndarray = np.ndarray
     for i, g in enumerate(gates):
-        e = arr[i]
-        e.kind = KIND[g.kind]
-        e.nt = len(g.targets)
-        e.nc = len(g.controls)
-        if e.nt > MAX_TARGETS or e.nc > MAX_CONTROLS:
+        t, c = g.targets, g.controls
+        nt, nc = len(t), len(c)
+        if nt > MAX_TARGETS or nc > MAX_CONTROLS:
             raise QJError(4, f"gate {i}: too many qubits")
-        for j, q in enumerate(g.targets):
-            e.targets[j] = int(q)
-        for j, q in enumerate(g.controls):
-            e.controls[j] = int(q)
-        if g.kind == "dense":
-            d = np.asarray(g.data[0], dtype=np_dtype).reshape(-1)
-        elif g.kind == "diag":
-            d = np.asarray(g.data[0], dtype=np_dtype).reshape(-1)
-        elif g.kind == "fsim":
-            d = np.asarray(list(np.asarray(g.data[0]).reshape(-1)) + [g.data[1]], dtype=np_dtype)
-        else:
-            d = None
-        if d is not None:
-            d = np.ascontiguousarray(d)
-            keep.append(d)
-            e.data = d.ctypes.data
-        else:
-            e.data = None
-    return arr, len(gates), keep
+        k = g.kind
+        kinds[i] = KIND[k]
+        nts[i] = nt
+        ncs[i] = nc
+        tg[MAX_TARGETS * i:MAX_TARGETS * i + nt] = t
+        if nc:
+            ct[MAX_CONTROLS * i:MAX_CONTROLS * i + nc] = c
+        if k == "dense" or k == "diag":
+            d = g.data[0]
+            if type(d) is not ndarray:
+                d = np.asarray(d)
+            parts.append(d)
+            owner.append(i)
+            lens.append(d.size)
+        elif k == "fsim":
+            d = np.append(np.asarray(g.data[0]).reshape(-1), g.data[1])
+            parts.append(d)
+            owner.append(i)
+            lens.append(d.size)
+    if ng:
+        rec["kind"][:ng] = kinds
+        rec["nt"][:ng] = nts
+        rec["nc"][:ng] = ncs
+        rec["targets"][:ng] = np.asarray(tg, dtype=np.int32).reshape(-1, MAX_TARGETS)[:ng]
+        rec["controls"][:ng] = np.asarray(ct, dtype=np.int32).reshape(-1, MAX_CONTROLS)[:ng]
+    coeff = None
+    if parts:
+        coeff = np.ascontiguousarray(np.concatenate(parts, axis=None).astype(np_dtype, copy=False))
+        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+        rec["data"][np.asarray(owner)] = np.uint64(coeff.ctypes.data) + offs * np.uint64(coeff.itemsize)
+    arr = rec.ctypes.data_as(ctypes.POINTER(qj_gate))
+    return arr, ng, (rec, coeff)
 
 
 def plan_circuit(n, nshards, gates, fuse=False, amp_bytes=16, max_steps=1 << 16):

@@ -170,11 +170,17 @@ def test_specialised_exact_every_position(dt):
 
 # ------------------------------------------------ circuits
 @pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
-@pytest.mark.parametrize("name", ["qft10", "variational12", "supremacy3x4", "qaoa10", "bv10", "random10"])
+@pytest.mark.parametrize("name", ["qft10", "variational12", "supremacy3x4", "qaoa10", "bv10", "random10",
+                                  "qft15", "variational16", "supremacy4x4", "qaoa16", "bv15", "random16"])
 def test_circuits_vs_oracle(dt, name):
+    """n <= 13 (c128) / 14 (c64) runs fused circuits as whole-state SMEM
+    programs; the larger cases exercise the window tile passes."""
     circ = {"qft10": lambda: C.qft(10), "variational12": lambda: C.variational(12, layers=3),
             "supremacy3x4": lambda: C.supremacy(3, 4, 12), "qaoa10": lambda: C.qaoa(10, 2),
-            "bv10": lambda: C.bv(10), "random10": lambda: C.random_circuit(10, 300, 3)}[name]()
+            "bv10": lambda: C.bv(10), "random10": lambda: C.random_circuit(10, 300, 3),
+            "qft15": lambda: C.qft(15), "variational16": lambda: C.variational(16, layers=3),
+            "supremacy4x4": lambda: C.supremacy(4, 4, 12), "qaoa16": lambda: C.qaoa(16, 2),
+            "bv15": lambda: C.bv(15), "random16": lambda: C.random_circuit(16, 300, 4)}[name]()
     n = circ.n
     rng = np.random.default_rng(11)
     psi = rand_state(n, rng, dt)
@@ -485,3 +491,36 @@ def test_tfim_adiabatic_ground_energy_gpu():
     H1 = E.tfim_hamiltonian(n, 1.0)
     e0 = np.linalg.eigvalsh(H1)[0]
     assert abs(E.energy(x.cpu().numpy(), H1) - e0) <= 0.02 * abs(e0)
+
+
+# ------------------------------------------------ whole-state SMEM programs (small states)
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+def test_small_state_programs_every_size(dt):
+    """QJ_FUSE on n <= 13 (c128) / 14 (c64): runs of gates execute as one
+    whole-state shared-memory program; dense gates on 5+ targets run as
+    ordinary passes in between.  Every size up to the SMEM limit, vs the oracle."""
+    nmax = 13 if dt == np.complex128 else 14
+    for n in range(1, nmax + 1):
+        rng = np.random.default_rng(500 + n)
+        circ = C.random_circuit(n, 80, 900 + n, max_targets=min(5, n), max_controls=min(2, max(0, n - 1)))
+        psi = rand_state(n, rng, dt)
+        x = to_gpu(psi, dt)
+        st = qjp.State(x, basis=None)
+        st.apply_circuit(circ.gates, fuse=True)
+        st.sync()
+        check_close(x.cpu().numpy(), oracle_circuit(circ, psi, dt), dt)
+
+
+def test_small_state_is_one_launch():
+    n = 10
+    circ = C.qft(n)
+    t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(t, basis=5)
+    st.counters(reset=True)
+    st.apply_circuit(circ.gates, fuse=True)
+    st.sync()
+    c = st.counters(reset=True)
+    assert c["launches"] == 1 and c["passes"] == 1
+    y = np.arange(2**n, dtype=np.uint64)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * ((5 * y) % 2**n).astype(np.float64) / 2**n)
+    assert np.max(np.abs(t.cpu().numpy() - exp)) < 1e-12
