@@ -96,6 +96,30 @@ qj_status qj_state_init(qj_state* out, void* amps_dev, int n, qj_dtype dt,
 qj_status qj_state_init_sharded(qj_state* out, void* const* shards, int nshards, int n,
                                 qj_dtype dt, uint64_t basis_index, void* cuda_stream);
 
+/* Host-staged state ("the full state vector is stored in
+ * the host memory ... only slices of it are transferred to the GPUs for
+ * calculation", with "a single GPU that is re-used for multiple state
+ * slices").  `amps_host` is caller-owned HOST memory of 2^n amplitudes
+ * (16-byte aligned; pin it -- cudaHostRegister / cudaMallocHost -- or copies
+ * cannot overlap), split into `nslices` (power of two) slices on the top
+ * log2(nslices) qubits.  The planner is the sharded one; each run of per-slice
+ * passes between global-qubit exchanges streams every slice through the GPU
+ * once (three slice buffers of 2^(n - log2 nslices) amplitudes in HBM, H2D /
+ * compute / D2H overlapped on separate streams).  A slice is held as two
+ * half-slices through a pointer table: a global-qubit exchange with the top
+ * local bit swaps table entries (no bytes move); one with a lower local bit L
+ * adds SWAP(L, top) passes to the neighbouring sweeps.  Results are bit
+ * identical to qj_state_init_sharded with the same slice count.  After
+ * exchanges the caller's buffer holds the half-slices in permuted order (like
+ * the permuted bit order of device states); qj_state_canonicalize restores
+ * the canonical layout (host block moves) and returns after the data is in
+ * place; otherwise the buffer is valid after qj_sync.  Plans are not cached.
+ * qj_probabilities' out_dev, qj_sample and qj_collapse work as for device
+ * states.  Errors: as qj_state_init_sharded; CUDA errors if the slice buffers
+ * do not fit the device. */
+qj_status qj_state_init_host(qj_state* out, void* amps_host, int n, qj_dtype dt, int nslices,
+                             uint64_t basis_index, void* cuda_stream);
+
 /* Re-initialise an existing handle to |basis_index> (QJ_KEEP: no-op). */
 qj_status qj_state_reset(qj_state s, uint64_t basis_index);
 
@@ -163,8 +187,8 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
  * so after qj_apply_circuit(QJ_FUSE) or on sharded states the amplitude
  * buffer may hold the state in a permuted bit order (qj_probabilities is
  * canonical regardless).  qj_state_canonicalize moves the data back to the
- * canonical order (R1) with SWAP passes / exchanges and resets the map.
- * Errors: UNSUPPORTED if two global bits would have to trade places. */
+ * canonical order (R1) with SWAP passes / exchanges (two global bits trade
+ * places by three exchanges through the top local bit) and resets the map. */
 qj_status qj_state_canonicalize(qj_state s);
 
 /* ---- readout -----------------------------------------------------------------

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "qj_internal.h"
@@ -62,6 +63,21 @@ struct qj_state_s {
     size_t xbuf_bytes = 0;
     void* mbuf = nullptr;  // measurement scratch (norm partials, sampler CDF); never in a captured graph
     size_t mbuf_bytes = 0;
+    // host-staged states (row f4): `shards` are HOST slices;
+    // work streams them through three device buffers (H2D / compute / D2H on
+    // separate streams).
+    bool host = false;
+    // half-slice table: logical slice r = halves[2r] (local top bit 0) and
+    // halves[2r+1] (top bit 1), each 2^(nl-1) amplitudes of the caller's buffer.
+    // Exchanges with the top local bit swap table entries (no data moves).
+    std::vector<void*> halves;
+    void* host_base = nullptr;
+    struct HostPipe {
+        bool ready = false;
+        void* dbuf[3] = {};
+        cudaStream_t h2d = nullptr, d2h = nullptr;
+        cudaEvent_t up[3] = {}, done[3] = {}, freed[3] = {}, mark = nullptr, tail = nullptr;
+    } hp;
     int total_shards() const { return comm ? nranks : (int)shards.size(); }
     // circuits seen before: plan + prepared tile passes (+ a CUDA graph)
     struct CachedPlan {
@@ -316,7 +332,232 @@ void* shard_ptr(qj_state s, int g) {
     return s->shards[(size_t)g];
 }
 
+// ---- host-staged execution -------------------------------------------------
+void host_identity_halves(qj_state s) {
+    const size_t hb = ((size_t)s->amp_bytes << s->nl) / 2;
+    s->halves.resize(2 * s->shards.size());
+    for (size_t h = 0; h < s->halves.size(); ++h) s->halves[h] = static_cast<unsigned char*>(s->host_base) + h * hb;
+}
+
+void copy_par(void* dst, const void* src, size_t bytes) {
+    const size_t kMin = 64ull << 20;
+    const unsigned nt = bytes < kMin ? 1u : std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+    if (nt == 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (bytes + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        const size_t b = t * per, e = std::min(bytes, b + per);
+        if (b >= e) break;
+        th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b); });
+    }
+    for (auto& x : th) x.join();
+}
+
+// Move the half-slices back to their canonical places in the caller's buffer
+// (cycle by cycle through one temporary half).  The stream must be idle.
+qj_status host_materialize(qj_state s) {
+    const size_t nh = s->halves.size();
+    const size_t hb = ((size_t)s->amp_bytes << s->nl) / 2;
+    auto home = [&](size_t h) { return static_cast<unsigned char*>(s->host_base) + h * hb; };
+    // where[h] = index of the home block currently holding logical half h's data
+    std::vector<size_t> where(nh);
+    for (size_t h = 0; h < nh; ++h) where[h] = (size_t)(static_cast<unsigned char*>(s->halves[h]) -
+                                                         static_cast<unsigned char*>(s->host_base)) / hb;
+    bool identity = true;
+    for (size_t h = 0; h < nh; ++h) identity &= where[h] == h;
+    if (identity) return QJ_OK;
+    std::vector<unsigned char> tmp;
+    try {
+        tmp.resize(hb);
+    } catch (...) {
+        return fail(QJ_ERR_CAPACITY, "host materialise: no memory for a %zu-byte temporary", hb);
+    }
+    std::vector<char> done(nh, 0);
+    for (size_t h = 0; h < nh; ++h) {
+        if (done[h] || where[h] == h) {
+            done[h] = 1;
+            continue;
+        }
+        // cycle: home(h) must receive block where[h]; save home(h) first
+        copy_par(tmp.data(), home(h), hb);
+        size_t cur = h;
+        // the block originally at home(h) belongs to logical half k with where[k] == h
+        while (true) {
+            const size_t src = where[cur];
+            done[cur] = 1;
+            if (src == h) {
+                copy_par(home(cur), tmp.data(), hb);
+                break;
+            }
+            copy_par(home(cur), home(src), hb);
+            cur = src;
+            // the data now needed at home(src) is logical half `src`'s, stored at where[src]
+        }
+    }
+    host_identity_halves(s);
+    return QJ_OK;
+}
+
+qj_status host_pipe_init(qj_state s) {
+    auto& p = s->hp;
+    if (p.ready) return QJ_OK;
+    const size_t bytes = (size_t)s->amp_bytes << s->nl;
+    cudaError_t e = cudaSuccess;
+    for (int b = 0; b < 3 && e == cudaSuccess; ++b) e = cudaMalloc(&p.dbuf[b], bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking);
+    for (int b = 0; b < 3 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&p.up[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.done[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.freed[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.mark, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.tail, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "host-staging pipeline setup (3 slice buffers)");
+    p.ready = true;
+    return QJ_OK;
+}
+
+// Stream the listed host slices through the device: slice t is uploaded on the
+// H2D stream into buffer t mod 3, `compute(r, dev_ptr)` is enqueued on the
+// handle's stream, and (write_back) the buffer is copied back on the D2H
+// stream, so upload, compute and download of consecutive slices overlap.  The
+// handle's stream waits for the last write-back, so anything enqueued on it
+// afterwards (and qj_sync) sees the updated host slices.
+template <typename F>
+qj_status host_sweep(qj_state s, const std::vector<int>& slices, bool write_back, F&& compute) {
+    if (slices.empty()) return QJ_OK;
+    if (qj_status q = host_pipe_init(s)) return q;
+    auto& p = s->hp;
+    const size_t bytes = (size_t)s->amp_bytes << s->nl;
+    cudaError_t e = cudaEventRecord(p.mark, s->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p.h2d, p.mark, 0);
+    bool used[3] = {false, false, false};
+    for (size_t t = 0; t < slices.size() && e == cudaSuccess; ++t) {
+        const int b = (int)(t % 3);
+        const int r = slices[t];
+        if (used[b]) e = cudaStreamWaitEvent(p.h2d, p.freed[b], 0);
+        const size_t hb = bytes / 2;
+        unsigned char* db = static_cast<unsigned char*>(p.dbuf[b]);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(db, s->halves[2 * (size_t)r], hb, cudaMemcpyHostToDevice, p.h2d);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(db + hb, s->halves[2 * (size_t)r + 1], hb, cudaMemcpyHostToDevice, p.h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(p.up[b], p.h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, p.up[b], 0);
+        if (e == cudaSuccess) e = compute(r, p.dbuf[b]);
+        if (e != cudaSuccess) break;
+        if (write_back) {
+            e = cudaEventRecord(p.done[b], s->stream);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(p.d2h, p.done[b], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(s->halves[2 * (size_t)r], db, hb, cudaMemcpyDeviceToHost, p.d2h);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(s->halves[2 * (size_t)r + 1], db + hb, hb, cudaMemcpyDeviceToHost, p.d2h);
+            if (e == cudaSuccess) e = cudaEventRecord(p.freed[b], p.d2h);
+        } else {
+            e = cudaEventRecord(p.freed[b], s->stream);
+        }
+        used[b] = true;
+    }
+    if (e == cudaSuccess && write_back) {
+        e = cudaEventRecord(p.tail, p.d2h);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, p.tail, 0);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "host-staged sweep");
+    return QJ_OK;
+}
+
+qj_status run_step_on(qj_state s, const Step& st, void* ptr) {
+    if (st.type == Step::PASS && st.pass.k > 5 && st.pass.kind == PK_DENSE) {
+        const size_t need = (size_t)s->amp_bytes * ((size_t)1 << (2 * st.pass.k));
+        if (qj_status q = ensure_scratch(s, need)) return q;
+    }
+    ProfScope prof(s, prof_kind(st), st.alg_bytes);
+    cudaError_t e = by_dtype(s->dt, [&](auto z) {
+        using R = decltype(z);
+        if (st.type == Step::TILE) return run_tile<R>(st.tile, ptr, s->nl, s->stream, s->stg, s->ls);
+        if (st.type == Step::SMALL) return run_small<R>(st.prog, ptr, s->nl, s->stream, s->ls);
+        return run_pass<R>(st.pass, ptr, s->nl, s->stream, s->scratch, s->scratch_bytes, s->ls);
+    });
+    if (e != cudaSuccess) return cuda_fail(e, "pass launch");
+    s->ctr.passes++;
+    s->ctr.alg_bytes += st.alg_bytes;
+    return QJ_OK;
+}
+
+// Runs of per-slice steps between exchanges execute as ONE sweep over the
+// slices (each slice uploaded once, all its steps applied, written back once).
+// An exchange uploads each slice pair, swaps the halves in HBM and writes both
+// back.  Bit for bit the same kernels as the in-HBM sharded path.
+qj_status execute_host(qj_state s, const std::vector<Step>& steps_in) {
+    const size_t nsh = s->shards.size();
+    // exchanges with a lower local bit L: SWAP(L, top) on every slice, the
+    // zero-copy exchange with the top bit, SWAP(L, top) again (the SWAP passes
+    // join the neighbouring sweeps)
+    std::vector<Step> steps;
+    for (const Step& st : steps_in) {
+        if (st.type != Step::EXCHANGE || st.lbit == s->nl - 1) {
+            steps.push_back(st);
+            continue;
+        }
+        auto swaps = [&]() {
+            for (size_t r = 0; r < nsh; ++r) {
+                Step w;
+                w.type = Step::PASS;
+                w.shard = (int)r;
+                w.pass.kind = PK_SWAP;
+                w.pass.k = 2;
+                w.pass.tpos[0] = st.lbit;
+                w.pass.tpos[1] = s->nl - 1;
+                w.alg_bytes = pass_alg_bytes(w.pass, s->nl, s->amp_bytes);
+                steps.push_back(std::move(w));
+            }
+        };
+        swaps();
+        Step x = st;
+        x.lbit = s->nl - 1;
+        steps.push_back(x);
+        swaps();
+    }
+    size_t i = 0;
+    while (i < steps.size()) {
+        if (steps[i].type == Step::EXCHANGE) {
+            // global bit j <-> top local bit: relabel half-slices (zero copy)
+            const Step& st = steps[i++];
+            for (size_t r = 0; r < nsh; ++r) {
+                if ((r >> st.gbit) & 1) continue;
+                const size_t r2 = r | (1ull << st.gbit);
+                std::swap(s->halves[2 * r + 1], s->halves[2 * r2]);
+            }
+            s->ctr.exchanges++;
+            continue;
+        }
+        size_t j = i;
+        while (j < steps.size() && steps[j].type != Step::EXCHANGE) ++j;
+        std::vector<std::vector<size_t>> per(nsh);
+        for (size_t k = i; k < j; ++k)
+            if (steps[k].shard >= 0 && (size_t)steps[k].shard < nsh) per[(size_t)steps[k].shard].push_back(k);
+        std::vector<int> slices;
+        for (size_t r = 0; r < nsh; ++r)
+            if (!per[r].empty()) slices.push_back((int)r);
+        qj_status inner = QJ_OK;
+        qj_status q = host_sweep(s, slices, true, [&](int r, void* dptr) -> cudaError_t {
+            for (size_t k : per[(size_t)r])
+                if ((inner = run_step_on(s, steps[k], dptr)) != QJ_OK) return cudaErrorUnknown;
+            return cudaSuccess;
+        });
+        if (inner != QJ_OK) return inner;
+        if (q != QJ_OK) return q;
+        i = j;
+    }
+    s->ctr.launches = s->ls.launches;
+    return QJ_OK;
+}
+
 qj_status execute(qj_state s, const std::vector<Step>& steps) {
+    if (s->host) return execute_host(s, steps);
     cudaError_t e = cudaSuccess;
     for (const Step& st : steps) {
         if (st.type == Step::EXCHANGE) {
@@ -463,7 +704,7 @@ void account(qj_state s, const qj_state_s::CachedPlan& p) {
 qj_status apply_circuit_cached(qj_state s, const qj_gate* gates, int ngates, uint32_t flags,
                                const std::vector<LGate>& gs, bool* done) {
     *done = false;
-    if (!s->cache_on || s->comm) return QJ_OK;
+    if (!s->cache_on || s->comm || s->host) return QJ_OK;
     std::vector<uint64_t> key = plan_key(s, gates, ngates, flags);
     for (size_t i = 0; i < s->plans.size(); ++i) {
         qj_state_s::CachedPlan* p = s->plans[i];
@@ -576,7 +817,7 @@ uint64_t qj_insert_zero_bits(uint64_t g, const int* sorted_pos, int npos) {
 
 static qj_status init_common(qj_state* out, void* const* shards, int nshards, int n, qj_dtype dt,
                              uint64_t basis_index, void* cuda_stream, void* comm = nullptr, int rank = 0,
-                             int nranks = 1) {
+                             int nranks = 1, bool host = false) {
     if (!out) return fail(QJ_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (!dtype_ok(dt)) return fail(QJ_ERR_DTYPE, "unknown dtype %d", (int)dt);
@@ -607,6 +848,7 @@ static qj_status init_common(qj_state* out, void* const* shards, int nshards, in
     s->comm = comm;
     s->rank = rank;
     s->nranks = nranks;
+    s->host = host;
     s->phys.resize(n);
     for (int q = 0; q < n; ++q) s->phys[q] = n - 1 - q;  // reading R1
     *out = s;
@@ -640,6 +882,34 @@ qj_status qj_state_init_sharded(qj_state* out, void* const* shards, int nshards,
     return init_common(out, shards, nshards, n, dt, basis_index, cuda_stream);
 }
 
+qj_status qj_state_init_host(qj_state* out, void* amps_host, int n, qj_dtype dt, int nslices, uint64_t basis_index,
+                             void* cuda_stream) {
+    if (!out) return fail(QJ_ERR_INVALID_ARG, "out is NULL");
+    if (!dtype_ok(dt)) return fail(QJ_ERR_DTYPE, "unknown dtype %d", (int)dt);
+    if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
+    if (nslices < 1 || (nslices & (nslices - 1))) return fail(QJ_ERR_INVALID_ARG, "nslices=%d is not a power of two", nslices);
+    if (!amps_host) return fail(QJ_ERR_INVALID_ARG, "amplitude buffer is NULL");
+    int g = 0;
+    while ((1 << g) < nslices) ++g;
+    if (g >= n) return fail(QJ_ERR_CAPACITY, "%d slices need more than n=%d qubits", nslices, n);
+    const size_t amp = dt == QJ_C64 ? 8 : 16;
+    const size_t slice = amp << (n - g);
+    std::vector<void*> sl((size_t)nslices);
+    for (int r = 0; r < nslices; ++r) sl[(size_t)r] = static_cast<unsigned char*>(amps_host) + (size_t)r * slice;
+    qj_status st = init_common(out, sl.data(), nslices, n, dt, QJ_KEEP, cuda_stream, nullptr, 0, 1, true);
+    if (st != QJ_OK) return st;
+    (*out)->host_base = amps_host;
+    host_identity_halves(*out);
+    if (basis_index != QJ_KEEP) {
+        st = qj_state_reset(*out, basis_index);
+        if (st != QJ_OK) {
+            qj_state_free(*out);
+            *out = nullptr;
+        }
+    }
+    return st;
+}
+
 qj_status qj_state_reset(qj_state s, uint64_t basis_index) {
     if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
     if (basis_index == QJ_KEEP) return QJ_OK;
@@ -648,6 +918,22 @@ qj_status qj_state_reset(qj_state s, uint64_t basis_index) {
     for (int q = 0; q < s->n; ++q) s->phys[q] = s->n - 1 - q;
     const uint64_t owner = basis_index >> s->nl;
     const uint64_t local = basis_index & ((1ull << s->nl) - 1);
+    if (s->host) {  // host slices: wait for in-flight write-backs, then fill on the host
+        cudaError_t e = cudaStreamSynchronize(s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "host reset sync");
+        host_identity_halves(s);
+        const size_t bytes = (size_t)s->amp_bytes << s->nl;
+        for (size_t i = 0; i < s->shards.size(); ++i) std::memset(s->shards[i], 0, bytes);
+        unsigned char* p = static_cast<unsigned char*>(s->shards[(size_t)owner]) + local * (size_t)s->amp_bytes;
+        if (s->dt == QJ_C64) {
+            const float one[2] = {1.0f, 0.0f};
+            std::memcpy(p, one, sizeof(one));
+        } else {
+            const double one[2] = {1.0, 0.0};
+            std::memcpy(p, one, sizeof(one));
+        }
+        return QJ_OK;
+    }
     for (size_t i = 0; i < s->shards.size(); ++i) {
         const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
         cudaError_t e = by_dtype(s->dt, [&](auto z) {
@@ -715,6 +1001,20 @@ qj_status qj_state_free(qj_state s) {
     if (s->bins) cudaFree(s->bins);
     if (s->xbuf) cudaFree(s->xbuf);
     if (s->mbuf) cudaFree(s->mbuf);
+    if (s->hp.ready) {
+        cudaStreamSynchronize(s->hp.h2d);
+        cudaStreamSynchronize(s->hp.d2h);
+        for (int b = 0; b < 3; ++b) {
+            cudaFree(s->hp.dbuf[b]);
+            cudaEventDestroy(s->hp.up[b]);
+            cudaEventDestroy(s->hp.done[b]);
+            cudaEventDestroy(s->hp.freed[b]);
+        }
+        cudaEventDestroy(s->hp.mark);
+        cudaEventDestroy(s->hp.tail);
+        cudaStreamDestroy(s->hp.h2d);
+        cudaStreamDestroy(s->hp.d2h);
+    }
     delete s;
     return QJ_OK;
 }
@@ -825,24 +1125,33 @@ static qj_status marginal_bins(qj_state s, const int* qubits, int nq) {
     if (qj_status st = ensure_bins(s, nb)) return st;
     e = cudaMemsetAsync(s->bins, 0, nb * sizeof(double), s->stream);
     if (e != cudaSuccess) return cuda_fail(e, "bins memset");
-    for (size_t i = 0; i < s->shards.size(); ++i) {
+    auto one = [&](size_t i, const void* src) -> cudaError_t {
         const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
         int pos[64], gv[64];
-        for (int i = 0; i < nq; ++i) {
-            const int b = s->phys[qubits[i]];
+        for (int k = 0; k < nq; ++k) {
+            const int b = s->phys[qubits[k]];
             if (b < nl) {
-                pos[i] = b;
-                gv[i] = 0;
+                pos[k] = b;
+                gv[k] = 0;
             } else {
-                pos[i] = -1;
-                gv[i] = (int)((r >> (b - nl)) & 1u);
+                pos[k] = -1;
+                gv[k] = (int)((r >> (b - nl)) & 1u);
             }
         }
-        e = by_dtype(s->dt, [&](auto z) {
+        return by_dtype(s->dt, [&](auto z) {
             using R = decltype(z);
-            return run_prob_marginal<R>(s->shards[i], nl, pos, gv, nq, s->bins, s->stream, s->ls);
+            return run_prob_marginal<R>(src, nl, pos, gv, nq, s->bins, s->stream, s->ls);
         });
-        if (e != cudaSuccess) return cuda_fail(e, "marginal launch");
+    };
+    if (s->host) {
+        std::vector<int> all(s->shards.size());
+        for (size_t i = 0; i < all.size(); ++i) all[i] = (int)i;
+        if (qj_status q = host_sweep(s, all, false, [&](int r, void* d) { return one((size_t)r, d); })) return q;
+    } else {
+        for (size_t i = 0; i < s->shards.size(); ++i) {
+            e = one(i, s->shards[i]);
+            if (e != cudaSuccess) return cuda_fail(e, "marginal launch");
+        }
     }
     if (s->comm) {  // sum the per-rank fp64 bins across ranks
         const char* why = nullptr;
@@ -866,24 +1175,32 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
         const size_t rb = s->dt == QJ_C64 ? 4 : 8;
         if (s->comm && !identity)
             return fail(QJ_ERR_UNSUPPORTED, "full probabilities of a remapped NCCL-sharded state: call qj_state_canonicalize first");
-        for (size_t i = 0; i < s->shards.size(); ++i) {
+        auto one = [&](size_t i, const void* src) -> cudaError_t {
             const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
             if (identity) {
                 // NCCL-sharded: out_dev holds this rank's 2^n_local values
                 void* dst = static_cast<unsigned char*>(out_dev) + (s->comm ? 0 : rb * (r << nl));
-                e = by_dtype(s->dt, [&](auto z) {
+                return by_dtype(s->dt, [&](auto z) {
                     using R = decltype(z);
-                    return run_prob_full<R>(s->shards[i], nl, dst, s->stream, s->ls);
-                });
-            } else {
-                int cpos[64];
-                for (int q = 0; q < n; ++q) cpos[s->phys[q]] = n - 1 - q;
-                e = by_dtype(s->dt, [&](auto z) {
-                    using R = decltype(z);
-                    return run_prob_scatter<R>(s->shards[i], nl, r, n, cpos, out_dev, s->stream, s->ls);
+                    return run_prob_full<R>(src, nl, dst, s->stream, s->ls);
                 });
             }
-            if (e != cudaSuccess) return cuda_fail(e, "probabilities launch");
+            int cpos[64];
+            for (int q = 0; q < n; ++q) cpos[s->phys[q]] = n - 1 - q;
+            return by_dtype(s->dt, [&](auto z) {
+                using R = decltype(z);
+                return run_prob_scatter<R>(src, nl, r, n, cpos, out_dev, s->stream, s->ls);
+            });
+        };
+        if (s->host) {
+            std::vector<int> all(s->shards.size());
+            for (size_t i = 0; i < all.size(); ++i) all[i] = (int)i;
+            if (qj_status q = host_sweep(s, all, false, [&](int r, void* d) { return one((size_t)r, d); })) return q;
+        } else {
+            for (size_t i = 0; i < s->shards.size(); ++i) {
+                e = one(i, s->shards[i]);
+                if (e != cudaSuccess) return cuda_fail(e, "probabilities launch");
+            }
         }
         s->ctr.launches = s->ls.launches;
         return QJ_OK;
@@ -942,19 +1259,27 @@ qj_status qj_collapse(qj_state s, const int* qubits, int nq, uint64_t outcome, d
     double* outs = partial + kPartials;
     cudaError_t e = cudaSuccess;
     std::vector<char> match(nsh);
+    std::vector<int> matching;
+    auto norm_one = [&](size_t i, const void* src) -> cudaError_t {
+        return by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            return run_subspace_norm<R>(src, nl, pos, val, m, partial, outs + i, s->stream, s->ls);
+        });
+    };
     for (size_t i = 0; i < nsh; ++i) {
         const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
         match[i] = (r & gmask) == gwant;
         if (match[i]) {
-            e = by_dtype(s->dt, [&](auto z) {
-                using R = decltype(z);
-                return run_subspace_norm<R>(s->shards[i], nl, pos, val, m, partial, outs + i, s->stream, s->ls);
-            });
+            matching.push_back((int)i);
+            e = s->host ? cudaSuccess : norm_one(i, s->shards[i]);
         } else {
             e = cudaMemsetAsync(outs + i, 0, sizeof(double), s->stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "collapse norm");
     }
+    if (s->host)
+        if (qj_status q = host_sweep(s, matching, false, [&](int r, void* d) { return norm_one((size_t)r, d); }))
+            return q;
     if (s->comm) {
         const char* why = nullptr;
         const NcclApi* api = nccl_api(&why);
@@ -973,16 +1298,24 @@ qj_status qj_collapse(qj_state s, const int* qubits, int nq, uint64_t outcome, d
     if (!(P > 1e-14)) return fail(QJ_ERR_ZERO_PROBABILITY, "P(outcome=%llu) = %.3e <= 1e-14", (unsigned long long)outcome, P);
     const double scale = 1.0 / std::sqrt(P);
     const size_t bytes = ((size_t)s->amp_bytes) << nl;
-    for (size_t i = 0; i < nsh; ++i) {
-        if (match[i]) {
-            e = by_dtype(s->dt, [&](auto z) {
-                using R = decltype(z);
-                return run_collapse_apply<R>(s->shards[i], nl, mask, want, scale, s->stream, s->ls);
-            });
-        } else {
-            e = cudaMemsetAsync(s->shards[i], 0, bytes, s->stream);
+    auto apply_one = [&](const void* dst) -> cudaError_t {
+        return by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            return run_collapse_apply<R>(const_cast<void*>(dst), nl, mask, want, scale, s->stream, s->ls);
+        });
+    };
+    if (s->host) {  // non-matching slices are zeroed on the host (the stream is idle here)
+        for (size_t i = 0; i < nsh; ++i)
+            if (!match[i]) {
+                std::memset(s->halves[2 * i], 0, bytes / 2);
+                std::memset(s->halves[2 * i + 1], 0, bytes / 2);
+            }
+        if (qj_status q = host_sweep(s, matching, true, [&](int, void* d) { return apply_one(d); })) return q;
+    } else {
+        for (size_t i = 0; i < nsh; ++i) {
+            e = match[i] ? apply_one(s->shards[i]) : cudaMemsetAsync(s->shards[i], 0, bytes, s->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "collapse apply");
         }
-        if (e != cudaSuccess) return cuda_fail(e, "collapse apply");
     }
     s->ctr.launches = s->ls.launches;
     return QJ_OK;
@@ -1203,7 +1536,15 @@ qj_status qj_state_canonicalize(qj_state s) {
                 steps.push_back(std::move(st));
             }
         } else if (cur >= nl && want >= nl) {
-            return fail(QJ_ERR_UNSUPPORTED, "canonicalize: global bits %d and %d would have to trade places", cur, want);
+            // two global bits trade places: (a L)(b L)(a L) = (a b) through the
+            // top local bit (zero-copy relabels for host-staged states)
+            for (int t = 0; t < 3; ++t) {
+                Step st;
+                st.type = Step::EXCHANGE;
+                st.gbit = (t == 1 ? want : cur) - nl;
+                st.lbit = nl - 1;
+                steps.push_back(std::move(st));
+            }
         } else {
             Step st;
             st.type = Step::EXCHANGE;
@@ -1216,6 +1557,11 @@ qj_status qj_state_canonicalize(qj_state s) {
     }
     qj_status st = execute(s, steps);
     if (st == QJ_OK) s->phys = phys;
+    if (st == QJ_OK && s->host) {  // put the half-slices back in the caller's buffer order
+        cudaError_t e = cudaStreamSynchronize(s->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "canonicalize sync");
+        st = host_materialize(s);
+    }
     return st;
 }
 

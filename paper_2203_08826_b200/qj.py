@@ -36,7 +36,7 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
            "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
            "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit", "qj_collapse",
-           "qj_sample_distribution", "qj_sample", "qj_measure"]
+           "qj_sample_distribution", "qj_sample", "qj_measure", "qj_state_init_host"]
 
 
 class QJError(RuntimeError):
@@ -122,6 +122,7 @@ def lib():
         "qj_fuse_circuit": ([I, ctypes.POINTER(qj_gate), I, I, ctypes.POINTER(qj_gate), ctypes.POINTER(ctypes.c_double),
                              I, IP, IP], S),
         "qj_collapse": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_double)], S),
+        "qj_state_init_host": ([ctypes.POINTER(P), P, I, I, I, U64, P], S),
         "qj_sample_distribution": ([P, I, U64, U64, ctypes.POINTER(qj_sample_opts), P, P, P], S),
         "qj_sample": ([P, IP, I, U64, U64, ctypes.POINTER(qj_sample_opts), P, P], S),
         "qj_measure": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double)], S),
@@ -369,6 +370,35 @@ class State:
         _check(L.qj_state_init(ctypes.byref(self._h), ctypes.c_void_p(tensor.data_ptr()), n, self.dtype,
                                ctypes.c_uint64(QJ_KEEP if basis is None else int(basis)),
                                ctypes.c_void_p(self.stream.cuda_stream), ctypes.c_void_p(comm)))
+        return self
+
+    @classmethod
+    def host(cls, tensor, nslices, basis=0, stream=None, device=None):
+        """Host-staged state: `tensor` is a contiguous
+        complex64/complex128 CPU tensor of 2^n amplitudes (pin it for
+        overlapped copies); the library streams its `nslices` slices through
+        the GPU.  Read the tensor only after sync()."""
+        import torch
+
+        if tensor.is_cuda or not tensor.is_contiguous():
+            raise ValueError("a host-staged state needs a contiguous CPU tensor")
+        if tensor.dtype not in (torch.complex64, torch.complex128):
+            raise ValueError("state tensors must be complex64 or complex128")
+        n = int(tensor.numel()).bit_length() - 1
+        if (1 << n) != tensor.numel():
+            raise ValueError("state length must be a power of two")
+        self = cls.__new__(cls)
+        self._h = ctypes.c_void_p()
+        self.dtype = QJ_C64 if tensor.dtype == torch.complex64 else QJ_C128
+        self.np_dtype = np.complex64 if self.dtype == QJ_C64 else np.complex128
+        self.real_dtype = torch.float32 if self.dtype == QJ_C64 else torch.float64
+        self.n = n
+        self.shards = [tensor]
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(lib().qj_state_init_host(ctypes.byref(self._h), ctypes.c_void_p(tensor.data_ptr()), n, self.dtype,
+                                        int(nslices), ctypes.c_uint64(QJ_KEEP if basis is None else int(basis)),
+                                        ctypes.c_void_p(self.stream.cuda_stream)))
         return self
 
     # -- lifetime ----------------------------------------------------------

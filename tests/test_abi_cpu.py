@@ -212,3 +212,19 @@ def test_measurement_validation_codes():
     with pytest.raises(ValueError):
         Q.sample_opts("gibbs")
     assert L.qj_state_free(h) == 0
+
+
+def test_host_state_init_validation():
+    L = Q.lib()
+    h = ctypes.c_void_p()
+    buf = (ctypes.c_double * 64)()
+    P = ctypes.cast(buf, ctypes.c_void_p)
+    K = ctypes.c_uint64(Q.QJ_KEEP)
+    assert L.qj_state_init_host(None, P, 4, 1, 2, K, None) == 1
+    assert L.qj_state_init_host(ctypes.byref(h), None, 4, 1, 2, K, None) == 1
+    assert L.qj_state_init_host(ctypes.byref(h), P, 4, 7, 2, K, None) == 6
+    assert L.qj_state_init_host(ctypes.byref(h), P, 4, 1, 3, K, None) == 1
+    assert L.qj_state_init_host(ctypes.byref(h), P, 4, 1, 16, K, None) == 5
+    assert L.qj_state_init_host(ctypes.byref(h), P, 41, 1, 2, K, None) == 5
+    assert L.qj_state_init_host(ctypes.byref(h), P, 4, 1, 2, K, None) == 0
+    assert L.qj_state_free(h) == 0

@@ -524,3 +524,79 @@ def test_small_state_is_one_launch():
     y = np.arange(2**n, dtype=np.uint64)
     exp = 2 ** (-n / 2) * np.exp(2j * np.pi * ((5 * y) % 2**n).astype(np.float64) / 2**n)
     assert np.max(np.abs(t.cpu().numpy() - exp)) < 1e-12
+
+
+# ------------------------------------------------ f4: host-staged states
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("nslices", [1, 2, 8])
+def test_host_staged_vs_oracle_and_sharded(dt, nslices):
+    """State in (pinned) host memory, slices streamed through the GPU
+    (PAPER.md:469-479): matches the oracle, and is bit-identical to the in-HBM
+    virtual-sharded path with the same slice count (same plan, same kernels)."""
+    n = 14
+    circ = C.random_circuit(n, 200, 31, max_targets=3, max_controls=2)
+    circ.gates += C.qft(n).gates
+    rng = np.random.default_rng(77)
+    psi = rand_state(n, rng, dt)
+    h = torch.from_numpy(psi.copy()).pin_memory()
+    st = qjp.State.host(h, nslices, basis=None)
+    st.apply_circuit(circ.gates, fuse=True)
+    pf = st.probabilities([0, 5, n - 1]).cpu().numpy()
+    st.canonicalize()
+    st.sync()
+    got = h.numpy().copy()
+    exp = oracle_circuit(circ, psi, dt)
+    check_close(got, exp, dt)
+    assert np.max(np.abs(pf - oracle.probabilities(exp, n, [0, 5, n - 1]))) < TOL[dt]
+    if nslices > 1:
+        parts = [torch.from_numpy(c.copy()).cuda() for c in np.split(psi, nslices)]
+        sh = qjp.State.sharded(parts, n, basis=None)
+        sh.apply_circuit(circ.gates, fuse=True)
+        sh.canonicalize()
+        sh.sync()
+        ref = np.concatenate([t.cpu().numpy() for t in parts])
+        assert np.array_equal(got, ref), "host-staged != in-HBM sharded"
+
+
+def test_host_staged_measurement_and_reset():
+    from oracle import measure as M
+    n = 12
+    psi = rand_state(n, np.random.default_rng(3), np.complex128)
+    h = torch.from_numpy(psi.copy()).pin_memory()
+    st = qjp.State.host(h, 4, basis=None)
+    p = st.collapse([0, 7], 2)
+    st.sync()
+    exp, pe = M.collapse(psi, n, [0, 7], 2)
+    assert abs(p - pe) < 1e-13
+    check_close(h.numpy().copy(), exp, np.complex128)
+    _, c = st.sample([7, 3], 20000, 5)
+    assert c.cpu().numpy().sum() == 20000
+    st.reset(0b101)
+    st.sync()
+    e = np.zeros(2**n)
+    e[0b101] = 1
+    assert np.array_equal(h.numpy().copy(), e.astype(np.complex128))
+
+
+@pytest.mark.parametrize("mode", ["sharded", "host"])
+@pytest.mark.parametrize("nshards", [4, 8])
+def test_canonicalize_global_bit_permutation(mode, nshards):
+    """QFT leaves global qubits permuted among themselves (its final SWAPs
+    pair top and bottom qubits); canonicalize restores them through three
+    exchanges per transposition."""
+    n = 14
+    x = 0b10110011101001
+    circ = C.qft(n)
+    if mode == "sharded":
+        parts = [torch.empty(2**n // nshards, dtype=torch.complex128, device="cuda") for _ in range(nshards)]
+        st = qjp.State.sharded(parts, n, basis=x)
+    else:
+        h = torch.empty(2**n, dtype=torch.complex128).pin_memory()
+        st = qjp.State.host(h, nshards, basis=x)
+    st.apply_circuit(circ.gates, fuse=True)
+    st.canonicalize()
+    st.sync()
+    got = np.concatenate([t.cpu().numpy() for t in parts]) if mode == "sharded" else h.numpy().copy()
+    y = np.arange(2**n, dtype=np.uint64)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * ((np.uint64(x) * y) % np.uint64(2**n)).astype(np.float64) / 2**n)
+    assert np.max(np.abs(got - exp)) < 1e-12

@@ -1,6 +1,9 @@
 """Run the tfim10 circuit through the whole-state SMEM kernel a few times
 (for ncu captures of small_kernel)."""
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 
