@@ -146,31 +146,42 @@ static bool nondiagonal(const LGate& g) {
     }
 }
 
-void Planner::plan_gate(const PlanContext& ctx, const LGate& g, std::vector<Step>& out) {
+bool needs_exchange(const PlanContext& ctx, const LGate& g) {
+    if (ctx.g == 0 || !nondiagonal(g)) return false;
+    for (int i = 0; i < g.nt; ++i)
+        if ((*ctx.phys)[g.t[i]] >= ctx.nl) return true;
+    return false;
+}
+
+// Bring every global target of a non-diagonal gate into the local bits:
+// EXCHANGE with the highest local bit the gate does not use; updates the map.
+void exchange_for(const PlanContext& ctx, const LGate& g, std::vector<Step>& out) {
     std::vector<int>& phys = *ctx.phys;
-    if (ctx.g > 0 && nondiagonal(g)) {
-        for (int i = 0; i < g.nt; ++i) {
-            const int b = phys[g.t[i]];
-            if (b < ctx.nl) continue;
-            // victim: highest local physical bit not used by this gate
-            int L = -1;
-            for (int cand = ctx.nl - 1; cand >= 0 && L < 0; --cand) {
-                bool used = false;
-                for (int j = 0; j < g.nt; ++j) used |= phys[g.t[j]] == cand;
-                for (int j = 0; j < g.nc; ++j) used |= phys[g.c[j]] == cand;
-                if (!used) L = cand;
-            }
-            Step s;
-            s.type = Step::EXCHANGE;
-            s.gbit = b - ctx.nl;
-            s.lbit = L;
-            out.push_back(s);
-            for (int q = 0; q < ctx.n; ++q) {
-                if (phys[q] == b) phys[q] = L;
-                else if (phys[q] == L) phys[q] = b;
-            }
+    if (!needs_exchange(ctx, g)) return;
+    for (int i = 0; i < g.nt; ++i) {
+        const int b = phys[g.t[i]];
+        if (b < ctx.nl) continue;
+        int L = -1;
+        for (int cand = ctx.nl - 1; cand >= 0 && L < 0; --cand) {
+            bool used = false;
+            for (int j = 0; j < g.nt; ++j) used |= phys[g.t[j]] == cand;
+            for (int j = 0; j < g.nc; ++j) used |= phys[g.c[j]] == cand;
+            if (!used) L = cand;
+        }
+        Step s;
+        s.type = Step::EXCHANGE;
+        s.gbit = b - ctx.nl;
+        s.lbit = L;
+        out.push_back(s);
+        for (int q = 0; q < ctx.n; ++q) {
+            if (phys[q] == b) phys[q] = L;
+            else if (phys[q] == L) phys[q] = b;
         }
     }
+}
+
+void Planner::plan_gate(const PlanContext& ctx, const LGate& g, std::vector<Step>& out) {
+    exchange_for(ctx, g, out);
     for (int r = 0; r < ctx.nshards; ++r) {
         Step s;
         s.type = Step::PASS;

@@ -53,6 +53,11 @@ class Planner {
     void plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates, std::vector<Step>& out);
 };
 
+// Sharded states: a non-diagonal gate with a target on a global bit first
+// swaps it into the local bits (EXCHANGE steps, map updated).
+bool needs_exchange(const PlanContext& ctx, const LGate& g);
+void exchange_for(const PlanContext& ctx, const LGate& g, std::vector<Step>& out);
+
 // The paper's greedy gate fusion into gates of <= max_qubits qubits
 // (fusion.cpp).
 std::vector<LGate> fuse_gates(const std::vector<LGate>& gates, int n, int max_qubits);

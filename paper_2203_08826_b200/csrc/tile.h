@@ -52,6 +52,7 @@ struct HOp {
     std::vector<HTerm> terms;   // RUN
 };
 struct TileSpec {
+    uint64_t gbase = 0;  // sharded states: (shard index) << n_local, OR-ed into predicate indices
     int w = 0;
     int wpos[TILE_W] = {};
     std::vector<TSeg> segs;

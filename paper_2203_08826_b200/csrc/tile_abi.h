@@ -100,6 +100,7 @@ struct TileArgs {
     const unsigned char* tables;  // device program buffer of this pass
     TileTablesLayout lay;
     uint64_t ntiles;
+    uint64_t gbase;  // global-bit part of the physical index (sharded states); predicates only
     int nseg, nops, nslots, pad;
     int wpos[TILE_W];  // ascending physical positions of the window bits
     TSeg seg[TILE_MAXSEG];

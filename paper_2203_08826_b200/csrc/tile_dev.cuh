@@ -379,11 +379,12 @@ __device__ __forceinline__ uint64_t tile_begin(const TileArgs<R>& a, uint64_t ti
     for (int i = 0; i < TILE_W; ++i) tb = insert_zero(tb, a.wpos[i]);
     const TSlot* slots = reinterpret_cast<const TSlot*>(a.tables + a.lay.slots);
     const TTerm<R>* terms = reinterpret_cast<const TTerm<R>*>(a.tables + a.lay.terms);
+    const uint64_t tg = tb | a.gbase;  // predicates see the global bits too
     for (int e = tid; e < a.nslots; e += TILE_THREADS) {
         Cx<R> p = cone<R>();
         const TSlot sl = slots[e];
         for (uint32_t t = sl.t0; t < sl.t1; ++t)
-            if ((tb & terms[t].cmask) == terms[t].cval) p = cmul(p, terms[t].f);
+            if ((tg & terms[t].cmask) == terms[t].cval) p = cmul(p, terms[t].f);
         tab[e] = p;
     }
     return tb;
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MINBLOCKS) tile_kernel(cons
         __syncthreads();  // tab ready
         for (int s = 0; s < a.nseg; ++s) {
             if (s > 0) tile_transpose(a, s, v, sm, tid);
-            const uint64_t tfull = tb | thread_phys(a, s, tid);
+            const uint64_t tfull = tb | a.gbase | thread_phys(a, s, tid);
             for (int o = a.seg[s].op0; o < a.seg[s].op1; ++o) apply_op(a, a.ops[o], v, tfull, tid, tab);
         }
         tile_store(a, a.nseg - 1, v, tb, tid);

@@ -69,6 +69,7 @@ bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned 
     std::memset(a, 0, sizeof(TileArgs<R>));
     if ((int)t.segs.size() < 1 || (int)t.segs.size() > TILE_MAXSEG) return false;
     a->ntiles = 1ull << (nl - TILE_W);
+    a->gbase = t.gbase;
     a->nseg = (int)t.segs.size();
     a->nops = (int)t.ops.size();
     uint64_t wmask = 0;

@@ -49,7 +49,7 @@ struct Item {
 
 struct PassBuild {
     std::vector<Item> items;
-    std::vector<Step> singles;  // each gate as a single-gate pass, converted at admission
+    std::vector<std::vector<Step>> singles;  // each gate as single-gate passes (one per shard it touches)
     uint64_t W = 0;
     int nops = 0, nmat = 0, nterms = 0, nnd = 0;  // nnd: non-diagonal ops (each may flush one run)
     double cost = 0;                               // estimated arithmetic per amplitude
@@ -249,7 +249,7 @@ static bool build_tile(const PassBuild& pb, int nl, int C, TileSpec& ts) {
 }
 
 void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates, std::vector<Step>& out) {
-    if (ctx.g > 0 || ctx.nl < TILE_W + 2) {
+    if (ctx.nl < TILE_W + 2) {
         for (const LGate& g : gates) plan_gate(ctx, g, out);
         return;
     }
@@ -263,7 +263,7 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
         if (pb.items.empty()) return;
         if (pb.singles.size() == 1) {
             // a single gate: the specialised single-gate pass touches fewer bytes
-            if (pb.singles[0].shard >= 0) out.push_back(pb.singles[0]);
+            for (const Step& st : pb.singles[0]) out.push_back(st);
         } else {
             Step s;
             s.type = Step::TILE;
@@ -282,23 +282,34 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
                     fprintf(stderr, " | %zu segs, %zu ops, %d runs, %d terms\n", s.tile.segs.size(),
                             s.tile.ops.size(), nruns, nterms);
                 }
-                out.push_back(std::move(s));
+                // one pass per shard: the same program, the shard's global bits
+                // enter the predicates through gbase (tile.h)
+                for (int r = 0; r < ctx.nshards; ++r) {
+                    Step sr = s;
+                    sr.shard = r;
+                    sr.tile.gbase = (uint64_t)r << ctx.nl;
+                    out.push_back(std::move(sr));
+                }
             } else {
                 // cannot happen with the limits below; stay correct anyway
-                for (const Step& st : pb.singles)
-                    if (st.shard >= 0) out.push_back(st);
+                for (const auto& v : pb.singles)
+                    for (const Step& st : v) out.push_back(st);
             }
         }
         pb = PassBuild();
         pb.W = low;
     };
     auto single = [&](const LGate& g) {
-        Step s;
-        s.type = Step::PASS;
-        s.shard = 0;
-        if (!specialise(ctx, g, 0, s.pass)) s.shard = -1;  // identity
-        else s.alg_bytes = pass_alg_bytes(s.pass, ctx.nl, ctx.amp_bytes);
-        return s;
+        std::vector<Step> v;
+        for (int r = 0; r < ctx.nshards; ++r) {
+            Step s;
+            s.type = Step::PASS;
+            s.shard = r;
+            if (!specialise(ctx, g, (uint64_t)r, s.pass)) continue;  // identity on this shard
+            s.alg_bytes = pass_alg_bytes(s.pass, ctx.nl, ctx.amp_bytes);
+            v.push_back(std::move(s));
+        }
+        return v;
     };
     // DAG-aware packing: a gate that does not fit the current pass is deferred
     // and blocks its qubits; later gates that depend on no deferred gate keep
@@ -347,6 +358,15 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
                 pb.items.push_back(std::move(it));
                 pb.singles.push_back(single(g));
                 continue;
+            }
+            if (needs_exchange(ctx, g)) {
+                // a global target: swap it into the local bits between passes
+                if (pb.items.empty() && deferred.empty()) {
+                    exchange_for(ctx, g, out);
+                } else {
+                    defer(idx);
+                    continue;
+                }
             }
             HOp op;
             if (!make_op(g, phys, op)) {
