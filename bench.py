@@ -309,7 +309,7 @@ def kinds_of(prof, steps, peak):
 
 def sharded_section(qj, torch, dev, world, rank, timeout_s, emit):
     """QFT(30 + log2 N) complex128 sharded over the N ranks (16 GiB per GPU):
-    global-qubit swaps run as NCCL exchanges.  One warm-up and one timed
+    fused tile passes per rank, global-qubit swaps as NCCL exchanges.  One warm-up and one timed
     circuit; a watchdog keeps a hang from losing the main line."""
     import threading
     from workloads import circuits as C
@@ -332,7 +332,7 @@ def sharded_section(qj, torch, dev, world, rank, timeout_s, emit):
         circ = C.qft(n)
         packed = st.pack_circuit(circ.gates)
         pb = torch.empty(1 << 10, dtype=torch.float64, device=dev)
-        st.apply_circuit(None, packed=packed)
+        st.apply_circuit(None, fuse=True, packed=packed)
         st.sync()
         st.reset(SEED_X)
         torch.cuda.synchronize(dev)
@@ -340,7 +340,7 @@ def sharded_section(qj, torch, dev, world, rank, timeout_s, emit):
         st.counters(reset=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        st.apply_circuit(None, packed=packed)
+        st.apply_circuit(None, fuse=True, packed=packed)
         st.probabilities(list(range(10)), out=pb)
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -352,7 +352,7 @@ def sharded_section(qj, torch, dev, world, rank, timeout_s, emit):
         res = {"workload": f"qft{n}_c128_sharded", "n": n, "ranks": world, "s_per_circuit": float(tt.item()) / 1e3,
                "exchanges": ctr["exchanges"], "exchange_bytes_per_rank": ctr["exchange_bytes"],
                "alg_bytes_per_rank": ctr["alg_bytes"], "marginal_sum": psum,
-               "note": "per-gate passes + NCCL local<->global swaps (fused planning is single-shard only)"}
+               "note": "fused window tile passes per rank + NCCL local<->global swaps between them"}
         st.free()
         return res
     except Exception as e:  # report, never lose the main line
