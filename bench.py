@@ -230,9 +230,12 @@ def timed_steps(torch, stream, steps, step, flush_buf):
     return sum(a.elapsed_time(b) for a, b in pairs)
 
 
-def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_gates=False):
+def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_gates=False, simulate=False):
     """Time `steps` steps (state reset + circuit + 10-qubit marginal) on the
-    device with CUDA events; returns timings, per-kind profile and counters."""
+    device with CUDA events; returns timings, per-kind profile and counters.
+    simulate=True runs the step as ONE qj_simulate call (the first tile pass
+    synthesises |basis>, the last one accumulates the marginal); otherwise as
+    qj_state_reset + qj_apply_circuit + qj_probabilities."""
     n = wl["n"]
     tdt = torch.complex128 if wl["dtype"] == "c128" else torch.complex64
     stream = torch.cuda.Stream(dev)
@@ -244,6 +247,9 @@ def measure(qj, torch, wl, fuse, steps, warmup, dev, world, profile=True, fuse_g
     pbuf = torch.empty(1 << len(readout), dtype=st.real_dtype, device=dev)
 
     def step():
+        if simulate:
+            st.simulate(wl["basis"], qubits=readout, fuse=fuse, fuse_gates=fuse_gates, packed=packed, out=pbuf)
+            return
         st.reset(wl["basis"])
         st.apply_circuit(None, fuse=fuse, packed=packed, fuse_gates=fuse_gates)
         st.probabilities(readout, out=pbuf)
@@ -379,8 +385,9 @@ def run_qj(args, rank, world):
     peak, peak_src = load_peaks()
     traffic, traffic_src = load_traffic()
 
-    # ---- headline: the default planner (fused window passes unless --no-fuse)
-    m = measure(qj, torch, wl, args.fuse, steps, args.warmup, dev, world)
+    # ---- headline: the default planner (fused window passes unless --no-fuse),
+    # the step as one qj_simulate call
+    m = measure(qj, torch, wl, args.fuse, steps, args.warmup, dev, world, simulate=args.fuse)
     st, psi, stream = m["st"], m["psi"], m["stream"]
 
     # ---- e2e: the public API with host buffers each step ----
@@ -399,9 +406,12 @@ def run_qj(args, rank, world):
         torch.distributed.barrier()
 
     def e2e_step():
-        st.reset(wl["basis"])
-        st.apply_circuit(gates, fuse=args.fuse)           # packs the host gate list each step
-        p = st.probabilities(readout, out=m["pbuf"])
+        if args.fuse:  # packs the host gate list each step
+            p = st.simulate(wl["basis"], gates, qubits=readout, fuse=True, out=m["pbuf"])
+        else:
+            st.reset(wl["basis"])
+            st.apply_circuit(gates, fuse=False)
+            p = st.probabilities(readout, out=m["pbuf"])
         with torch.cuda.stream(stream):
             host_out.copy_(p, non_blocking=True)
         stream.synchronize()
@@ -423,9 +433,24 @@ def run_qj(args, rank, world):
         mm = (np.uint64(wl["basis"]) * idx.astype(np.uint64)) % np.uint64(1 << n)
         exp = 2 ** (-n / 2) * np.exp(2j * np.pi * mm.astype(np.float64) / (1 << n))
         check = float(np.max(np.abs(got - exp)))
+        # |QFT|x>|^2 is uniform: every bin of the 10-qubit marginal is 2^-10
+        marg_err = float(np.max(np.abs(m["pbuf"].cpu().numpy() - 2.0 ** -len(wl["readout"]))))
+        check = max(check, marg_err)
     st.free()
     del psi, m["psi"]
     torch.cuda.empty_cache()
+
+    # ---- the same fused passes as three calls (reset + apply_circuit + probabilities) ----
+    separate = None
+    if args.fuse and not args.no_unfused:
+        sc = measure(qj, torch, wl, True, max(1, min(steps, 3)), 1, dev, world)
+        ss = max(1, min(steps, 3))
+        separate = {"value": sc["ms_max"] / 1e3 / (ss * world), "unit": "s/circuit", "steps": ss,
+                    "step": "qj_state_reset + qj_apply_circuit(QJ_FUSE) + qj_probabilities",
+                    "roofline": roofline_of(sc["prof"], sc["ms_prof"], peak, peak_src, traffic, traffic_src)}
+        sc["st"].free()
+        del sc
+        torch.cuda.empty_cache()
 
     # ---- per-gate passes (the north star's "per gate pass" bandwidth) ----
     unfused = None
@@ -474,7 +499,8 @@ def run_qj(args, rank, world):
         "data": "synthetic",
         "config": {"workload": args.workload, "n": n, "state": wl["dtype"], "gates": len(gates),
                    "basis": wl["basis"], "fuse": bool(args.fuse),
-                   "step": "state_reset + apply_circuit + 10-qubit marginal probabilities",
+                   "step": ("qj_simulate: state reset + apply_circuit + 10-qubit marginal probabilities in one call"
+                            if args.fuse else "state_reset + apply_circuit + 10-qubit marginal probabilities"),
                    "l2": (f"state {state_bytes >> 20} MiB >> 126 MB L2: inputs larger than L2, no flush"
                           if not needs_flush(wl) else
                           f"state {state_bytes >> 20} MiB fits L2: 256 MiB L2 flush before every timed step "
@@ -486,6 +512,7 @@ def run_qj(args, rank, world):
         "roofline": roofline_of(m["prof"], m["ms_prof"], peak, peak_src, traffic, traffic_src),
         "kinds": kinds_of(m["prof"], steps, peak),
         "profiled_ms_per_step": m["ms_prof"] / steps,
+        "separate_calls": separate,
         "unfused": unfused,
         "paper_fusion": paper,
         "cpu_baseline": cpu,

@@ -181,6 +181,23 @@ typedef struct {
  * before anything is enqueued. */
 qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_t flags);
 
+/* One simulation step in a single call: the same result as
+ *     qj_state_reset(s, basis); qj_apply_circuit(s, gates, ngates, flags);
+ *     qj_probabilities(s, qubits, nq, out_dev)   (skipped when nq == 0)
+ * with the state left in the buffer (possibly in a permuted bit order, as
+ * after qj_apply_circuit).  With QJ_FUSE on a single-device state (nq <= 10,
+ * JIT available) the library fuses the step's ends into its tile passes:
+ * the first pass synthesises |basis> in registers instead of reading an
+ * initialised buffer, and the last pass accumulates the fp64 marginal while
+ * it stores -- two fewer sweeps over the state.  Marginal sums are
+ * accumulated in a different order than qj_probabilities (agreement to fp64
+ * rounding).  Otherwise it runs the three calls.  Plans (and, from the
+ * second call on a non-default stream, a CUDA graph of the whole step) are
+ * cached per (circuit, flags, basis, qubits, out_dev).  Errors: as the three
+ * calls. */
+qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngates, uint32_t flags,
+                      const int* qubits, int nq, void* out_dev);
+
 /* Physical layout.  Qubit labels at this ABI are always logical: the handle
  * tracks a logical->physical bit map.  Fused circuits apply uncontrolled SWAP
  * gates as relabellings of that map and sharded states remap global qubits,

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "dist.h"
 #include "small.h"
+#include "tile_jit.h"
 
 using namespace qj;
 
@@ -86,6 +87,15 @@ struct qj_state_s {
         std::vector<int> phys_after;
         std::vector<PreparedTile> tiles;  // one per TILE step, in order
         std::vector<PreparedSmall> smalls;  // one per SMALL step, in order
+        // qj_simulate plans: |basis> synthesised by the first tile pass (else an
+        // init launch), the marginal fused into the last tile pass (else a
+        // marginal launch), bins owned by the plan
+        bool sim = false, init_first = false, marg_last = false;
+        uint64_t basis = 0;
+        int nq = 0;
+        int qpos[16] = {};
+        double* sim_bins = nullptr;
+        void* out = nullptr;
         cudaGraphExec_t exec = nullptr;
         bool graphable = true;
         uint64_t uses = 0, kernels = 0;
@@ -652,6 +662,7 @@ void release_plan(qj_state_s::CachedPlan* p) {
     if (p->exec) cudaGraphExecDestroy(p->exec);
     for (auto& t : p->tiles) tile_release(t);
     for (auto& t : p->smalls) small_release(t);
+    if (p->sim_bins) cudaFree(p->sim_bins);
     delete p;
 }
 
@@ -1401,6 +1412,199 @@ qj_status qj_measure(qj_state s, const int* qubits, int nq, uint64_t seed, uint6
     if (e != cudaSuccess) return cuda_fail(e, "measurement readback");
     *outcome_out = (uint64_t)h;
     return qj_collapse(s, qubits, nq, (uint64_t)h, prob_out);
+}
+
+// ------------------------------------------------------------------ qj_simulate
+static qj_status run_sim(qj_state s, qj_state_s::CachedPlan& p) {
+    cudaError_t e = cudaSuccess;
+    const size_t nb = p.nq > 0 ? (size_t)1 << p.nq : 0;
+    if (nb) e = cudaMemsetAsync(p.sim_bins, 0, nb * sizeof(double), s->stream);
+    if (e == cudaSuccess && p.init_first)
+        e = by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            return run_init<R>(s->shards[0], s->nl, p.basis, true, s->stream, s->ls);
+        });
+    if (e != cudaSuccess) return cuda_fail(e, "simulate prologue");
+    if (qj_status q = run_cached(s, p)) return q;
+    if (nb && !p.marg_last) {
+        int gv[16] = {};
+        e = by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            return run_prob_marginal<R>(s->shards[0], s->nl, p.qpos, gv, p.nq, p.sim_bins, s->stream, s->ls);
+        });
+        if (e != cudaSuccess) return cuda_fail(e, "simulate marginal");
+    }
+    if (nb) {
+        e = by_dtype(s->dt, [&](auto z) {
+            using R = decltype(z);
+            return run_bins_to_out<R>(p.sim_bins, nb, p.out, s->stream, s->ls);
+        });
+        if (e != cudaSuccess) return cuda_fail(e, "simulate readout");
+    }
+    return QJ_OK;
+}
+
+qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngates, uint32_t flags, const int* qubits,
+                      int nq, void* out_dev) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    if (s->n < 64 && basis >= (1ull << s->n))
+        return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "basis_index %llu >= 2^%d", (unsigned long long)basis, s->n);
+    if (ngates < 0 || (ngates > 0 && !gates)) return fail(QJ_ERR_INVALID_ARG, "bad gate list");
+    if (flags & ~(QJ_FUSE | QJ_FUSE_GATES)) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    if (nq < 0) return fail(QJ_ERR_INVALID_ARG, "nq=%d < 0", nq);
+    if (nq > 0) {
+        if (!out_dev) return fail(QJ_ERR_INVALID_ARG, "out_dev is NULL");
+        if (qj_status st = check_qubit_list(s, qubits, nq)) return st;
+    }
+    const bool fast = !s->comm && !s->host && s->shards.size() == 1 && (flags & QJ_FUSE) && nq <= 10 &&
+                      s->cache_on && tile_jit_available();
+    if (!fast) {  // the three calls it stands for
+        if (qj_status st = qj_state_reset(s, basis)) return st;
+        if (qj_status st = qj_apply_circuit(s, gates, ngates, flags)) return st;
+        return nq > 0 ? qj_probabilities(s, qubits, nq, out_dev) : QJ_OK;
+    }
+    std::vector<LGate> gs((size_t)ngates);
+    for (int i = 0; i < ngates; ++i) {
+        const qj_gate& g = gates[i];
+        if (g.nt > QJ_MAX_TARGETS || g.nc > QJ_MAX_CONTROLS)
+            return fail(QJ_ERR_TOO_MANY_TARGETS, "gate %d: nt=%d nc=%d exceeds the limits", i, g.nt, g.nc);
+        if (qj_status st = make_lgate(s, g.kind, g.targets, g.nt, g.controls, g.nc, g.data, gs[(size_t)i])) {
+            g_err = "gate " + std::to_string(i) + ": " + g_err;
+            return st;
+        }
+    }
+    for (int q = 0; q < s->n; ++q) s->phys[q] = s->n - 1 - q;  // the reset's map
+    std::vector<uint64_t> key = plan_key(s, gates, ngates, flags);
+    key.push_back(0x5117ull);
+    key.push_back(basis);
+    key.push_back((uint64_t)nq);
+    for (int i = 0; i < nq; ++i) key.push_back((uint64_t)qubits[i]);
+    key.push_back((uint64_t)(uintptr_t)out_dev);
+    qj_state_s::CachedPlan* p = nullptr;
+    for (size_t i = 0; i < s->plans.size() && !p; ++i)
+        if (s->plans[i]->key == key) {
+            p = s->plans[i];
+            std::rotate(s->plans.begin(), s->plans.begin() + (long)i, s->plans.begin() + (long)i + 1);
+        }
+    if (!p) {
+        if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, s->n, 2);
+        p = new qj_state_s::CachedPlan;
+        p->key.swap(key);
+        p->sim = true;
+        p->basis = basis;
+        p->nq = nq;
+        p->out = out_dev;
+        PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, 1, &s->phys};
+        s->planner.plan(ctx, gs, true, p->steps);
+        p->phys_after = s->phys;
+        for (int i = 0; i < nq; ++i) p->qpos[i] = p->phys_after[qubits[i]];
+        const bool first_tile = !p->steps.empty() && p->steps.front().type == Step::TILE;
+        const bool last_tile = !p->steps.empty() && p->steps.back().type == Step::TILE;
+        p->init_first = !first_tile;
+        if (first_tile) {
+            Step& f = p->steps.front();
+            f.tile.synth = true;
+            f.tile.synth_index = basis;
+            f.alg_bytes = (double)s->amp_bytes * std::ldexp(1.0, s->nl);  // writes only
+        }
+        if (nq > 0) {
+            cudaError_t e = cudaMalloc(&p->sim_bins, sizeof(double) << nq);
+            if (e != cudaSuccess) {
+                release_plan(p);
+                return cuda_fail(e, "simulate bins");
+            }
+        }
+        bool in_window = last_tile;
+        if (last_tile)
+            for (int i = 0; i < nq; ++i) {
+                bool w = false;
+                for (int j = 0; j < TILE_W; ++j) w |= p->steps.back().tile.wpos[j] == p->qpos[i];
+                in_window &= w;
+            }
+        if (nq > 0 && last_tile && in_window) {  // bins depend on (thread, register) only
+            Step& l = p->steps.back();
+            l.tile.nbins_q = nq;
+            for (int i = 0; i < nq; ++i) l.tile.bin_pos[i] = (int8_t)p->qpos[i];
+            l.tile.bins = p->sim_bins;
+            p->marg_last = true;
+        }
+        for (const Step& st : p->steps) {
+            if (st.type == Step::TILE) {
+                PreparedTile t;
+                cudaError_t e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return tile_prepare<R>(st.tile, s->shards[0], s->nl, t);
+                });
+                if (e != cudaSuccess || ((st.tile.synth || st.tile.nbins_q) && !t.jit)) {
+                    tile_release(t);
+                    release_plan(p);
+                    return e != cudaSuccess ? cuda_fail(e, "tile prepare") : fail(QJ_ERR_CUDA, "simulate: JIT unavailable");
+                }
+                p->tiles.push_back(std::move(t));
+            } else if (st.type == Step::SMALL) {
+                PreparedSmall t;
+                cudaError_t e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return small_prepare<R>(st.prog, s->shards[0], s->nl, t);
+                });
+                if (e != cudaSuccess) {
+                    small_release(t);
+                    release_plan(p);
+                    return cuda_fail(e, "small prepare");
+                }
+                p->smalls.push_back(t);
+            } else if (st.type == Step::PASS && st.pass.k > 5 && st.pass.kind == PK_DENSE) {
+                p->graphable = false;
+                const size_t need = (size_t)s->amp_bytes * ((size_t)1 << (2 * st.pass.k));
+                if (qj_status q = ensure_scratch(s, need)) {
+                    release_plan(p);
+                    return q;
+                }
+            }
+        }
+        s->plans.insert(s->plans.begin(), p);
+        while (s->plans.size() > 16) {
+            release_plan(s->plans.back());
+            s->plans.pop_back();
+        }
+        const uint64_t before = s->ls.launches;
+        if (qj_status q = run_sim(s, *p)) return q;
+        p->kernels = s->ls.launches - before;
+        p->uses = 1;
+    } else {
+        const uint64_t before = s->ls.launches;
+        const bool graph_ok = p->graphable && !s->profiling && s->stream != nullptr;
+        if (graph_ok && !p->exec) {
+            cudaGraph_t g = nullptr;
+            cudaError_t e = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal);
+            if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+            qj_status q = run_sim(s, *p);
+            e = cudaStreamEndCapture(s->stream, &g);
+            if (q != QJ_OK) return q;
+            if (e != cudaSuccess) return cuda_fail(e, "graph capture end");
+            e = cudaGraphInstantiate(&p->exec, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) {
+                p->exec = nullptr;
+                p->graphable = false;
+                cudaGetLastError();
+                return cuda_fail(e, "graph instantiate");
+            }
+            s->ls.launches = before;
+        }
+        if (graph_ok && p->exec) {
+            cudaError_t e = cudaGraphLaunch(p->exec, s->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+            s->ls.launches += p->kernels;
+        } else if (qj_status q = run_sim(s, *p)) {
+            return q;
+        }
+        p->uses++;
+    }
+    account(s, *p);
+    s->phys = p->phys_after;
+    s->ctr.launches = s->ls.launches;
+    return QJ_OK;
 }
 
 qj_status qj_fuse_circuit(int n, const qj_gate* in, int nin, int max_qubits, qj_gate* out, double* mats, int max_out,

@@ -53,6 +53,14 @@ struct HOp {
 };
 struct TileSpec {
     uint64_t gbase = 0;  // sharded states: (shard index) << n_local, OR-ed into predicate indices
+    // qj_simulate (JIT kernels only): the first pass can synthesise |basis>
+    // instead of loading, the last pass can accumulate the marginal of the
+    // listed physical bits (first = MSB of the bin index) into `bins`.
+    bool synth = false;
+    uint64_t synth_index = 0;
+    int nbins_q = 0;            // 0 = no fused marginal
+    int8_t bin_pos[16] = {};
+    double* bins = nullptr;
     int w = 0;
     int wpos[TILE_W] = {};
     std::vector<TSeg> segs;

@@ -17,7 +17,10 @@ constexpr int TILE_T = TILE_W - TILE_R;    // thread-index bits
 constexpr int TILE_THREADS = 1 << TILE_T;
 constexpr int TILE_NREG = 1 << TILE_R;
 constexpr int TILE_TCH = (TILE_T + 3) / 4;  // 4-bit chunks of the thread index
-constexpr int TILE_MINBLOCKS = 2;
+#ifndef QJ_TILE_MINBLOCKS
+#define QJ_TILE_MINBLOCKS 2
+#endif
+constexpr int TILE_MINBLOCKS = QJ_TILE_MINBLOCKS;  // resident CTAs per SM (JIT kernels: per-launch option)
 constexpr int TILE_MAXSEG = 8;
 constexpr int TILE_MAXOPS = 160;
 constexpr int TILE_MAXCX = 64;
@@ -25,6 +28,7 @@ constexpr int TILE_MAXRUNS = 96;
 constexpr int TILE_MAXSLOTS = 1024;
 constexpr int TILE_MAXTERMS = 1024;  // planner budget per pass
 constexpr int TILE_MAXMAT = 1024;    // complex entries in the matrix pool
+constexpr int TILE_MAXUC = 512;     // uniform coefficients staged in the kernel-parameter block (JIT)
 
 enum TOpType : uint8_t {
     TO_H = 0,     // Hadamard on R bit a
@@ -109,6 +113,16 @@ struct TileArgs {
     TOp ops[TILE_MAXOPS];
     uint64_t cx[TILE_MAXCX][2];
     TRunDesc runs[TILE_MAXRUNS];
+    // JIT kernels: tile-independent uniform coefficients (gate matrices, anchored
+    // phase factors, pattern tables) copied here at launch, so they are read
+    // through the constant bank instead of per-tile global loads
+    Cx<R> uc[TILE_MAXUC];
+    // qj_simulate fusions (JIT kernels; see tile.h)
+    uint64_t synth;          // local index of the basis amplitude (synthesised first pass)
+    double* bins;            // fused marginal: 2^nbq fp64 bins (global)
+    int nbq, fflags;         // fflags: 1 = synthesise the first load, 2 = fused marginal
+    int8_t bin_pos[16];      // physical bit of output bit k (k = 0 is the MSB)
+    uint16_t regbin[TILE_NREG];  // bin bits contributed by the last segment's register index
 };
 
 }  // namespace qj

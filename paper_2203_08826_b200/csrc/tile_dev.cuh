@@ -441,8 +441,12 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Issue the prefetch of `tile` into `sm` (no commit: the caller groups it).
 template <typename R>
-__device__ __forceinline__ void tile_prefetch(const TileArgs<R>& a, uint64_t tile, Cx<R>* sm, int tid) {
+__device__ __forceinline__ void tile_prefetch_issue(const TileArgs<R>& a, uint64_t tile, Cx<R>* sm, int tid) {
     uint64_t tb = tile;
 #pragma unroll
     for (int i = 0; i < TILE_W; ++i) tb = insert_zero(tb, a.wpos[i]);
@@ -470,7 +474,33 @@ __device__ __forceinline__ void tile_prefetch(const TileArgs<R>& a, uint64_t til
         if constexpr (sizeof(R) == 8) cp_async16(sm + y, psi + x);
         else cp_async8(sm + y, psi + x);
     }
+}
+
+template <typename R>
+__device__ __forceinline__ void tile_prefetch(const TileArgs<R>& a, uint64_t tile, Cx<R>* sm, int tid) {
+    tile_prefetch_issue(a, tile, sm, tid);
     cp_async_commit();
+}
+
+// Ring variant: tile i's data was committed as its own cp.async group; at most
+// N newer groups may still be in flight.
+template <int N, typename R>
+__device__ __forceinline__ void tile_load_ring(const TileArgs<R>& a, Cx<R> (&v)[TILE_NREG], const Cx<R>* sm, int tid) {
+    cp_async_wait_n<N>();
+    __syncthreads();
+    const TSeg& S = a.seg[0];
+    const uint32_t bl = swz<R>(thread_loc(a, 0, tid));
+    uint32_t sl[TILE_R];
+#pragma unroll
+    for (int j = 0; j < TILE_R; ++j) sl[j] = swz<R>(1u << S.rbits[j]);
+#pragma unroll
+    for (int r = 0; r < TILE_NREG; ++r) {
+        uint32_t y = bl;
+#pragma unroll
+        for (int j = 0; j < TILE_R; ++j)
+            if ((r >> j) & 1) y ^= sl[j];
+        v[r] = sm[y];
+    }
 }
 
 template <typename R>
@@ -491,6 +521,53 @@ __device__ __forceinline__ void tile_load_prefetched(const TileArgs<R>& a, Cx<R>
             if ((r >> j) & 1) y ^= sl[j];
         v[r] = sm[y];
     }
+}
+
+// qj_simulate: the first pass synthesises |basis> (no HBM read) ...
+template <typename R>
+__device__ __forceinline__ void tile_synth(const TileArgs<R>& a, Cx<R> (&v)[TILE_NREG], uint64_t tb, int tid) {
+    const TSeg& S = a.seg[0];
+    const uint64_t base = tb | thread_phys(a, 0, tid);
+    uint64_t rm[TILE_R];
+#pragma unroll
+    for (int j = 0; j < TILE_R; ++j) rm[j] = 1ull << a.wpos[S.rbits[j]];
+#pragma unroll
+    for (int r = 0; r < TILE_NREG; ++r) {
+        uint64_t x = base;
+#pragma unroll
+        for (int j = 0; j < TILE_R; ++j)
+            if ((r >> j) & 1) x |= rm[j];
+        v[r] = Cx<R>{x == a.synth ? R(1) : R(0), R(0)};
+    }
+}
+
+// ... and the last pass accumulates the marginal of the listed physical bits
+// (bin = tile part | thread part | register part, disjoint bit sets).
+__device__ __forceinline__ uint32_t bin_of(uint64_t x, const int8_t* pos, int nq) {
+    uint32_t b = 0;
+    for (int k = 0; k < nq; ++k) b = (b << 1) | (uint32_t)((x >> pos[k]) & 1u);
+    return b;
+}
+// Fused marginal, readout bits all inside the window: bin(thread, r) is
+// tile-independent, so each thread accumulates |v_r|^2 into its own SMEM slot
+// acc[r][tid] (no atomics); tile_bins_flush reduces them at the end.
+template <typename R>
+__device__ __forceinline__ void tile_bins(const Cx<R> (&v)[TILE_NREG], double* acc, int tid) {
+#pragma unroll
+    for (int r = 0; r < TILE_NREG; ++r)
+        acc[r * TILE_THREADS + tid] += (double)v[r].re * (double)v[r].re + (double)v[r].im * (double)v[r].im;
+}
+template <typename R>
+__device__ __forceinline__ void tile_bins_flush(const TileArgs<R>& a, const double* acc, double* sb, uint32_t thbin,
+                                                int tid) {
+    const int nb = 1 << a.nbq;
+    for (int i = tid; i < nb; i += TILE_THREADS) sb[i] = 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TILE_NREG; ++r) atomicAdd(&sb[thbin | a.regbin[r]], acc[r * TILE_THREADS + tid]);
+    __syncthreads();
+    for (int i = tid; i < nb; i += TILE_THREADS)
+        if (sb[i] != 0.0) atomicAdd(&a.bins[i], sb[i]);
 }
 
 // Registers of segment s-1 -> swizzled SMEM -> registers of segment s.

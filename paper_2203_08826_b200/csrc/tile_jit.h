@@ -9,11 +9,33 @@
 
 namespace qj {
 
-// Returns the CUfunction of the specialised kernel for this lowered pass
-// (compiling and caching it on first use), or nullptr with *err set when the
-// JIT is unavailable or disabled (QJ_JIT=0).  *compile_ms is set on a compile.
+#include <vector>
+
+// A compiled, circuit-specialised tile kernel and what its launch needs:
+// uniform coefficient slot j of TileArgs::uc takes fac[uc_src[j]] (>= 0) or
+// mats[-uc_src[j] - 1]; `npt` per-thread factor tables are staged in SMEM by
+// the kernel itself (launch with smem_extra more dynamic shared memory).
+struct JitKernel {
+    void* f = nullptr;
+    std::vector<int32_t> uc_src;
+    int npt = 0;
+    size_t smem_extra = 0;
+    int blocks = 2;  // resident CTAs per SM it was compiled for (grid = SMs x blocks)
+};
+
+// The specialised kernel for this lowered pass (compiled and cached on first
+// use; `blob` is the host copy of the pass's program buffer), or nullptr with
+// *err set when the JIT is unavailable or disabled (QJ_JIT=0).
 template <typename R>
-void* tile_jit_function(const TileArgs<R>& a, const void* mats_host, std::string* err, double* compile_ms);
+const JitKernel* tile_jit_kernel(const TileArgs<R>& a, const unsigned char* blob, std::string* err,
+                                 double* compile_ms);
+
+// Copy the kernel's uniform coefficients from the host program buffer into a->uc.
+template <typename R>
+void tile_jit_fill(const JitKernel& k, TileArgs<R>* a, const unsigned char* blob);
+
+// Whether JIT kernels can be built here (NVRTC + driver found, QJ_JIT != 0).
+bool tile_jit_available();
 
 cudaError_t tile_jit_launch(void* f, const void* args, unsigned grid, size_t smem, cudaStream_t st);
 

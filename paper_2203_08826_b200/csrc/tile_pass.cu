@@ -70,6 +70,22 @@ bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned 
     if ((int)t.segs.size() < 1 || (int)t.segs.size() > TILE_MAXSEG) return false;
     a->ntiles = 1ull << (nl - TILE_W);
     a->gbase = t.gbase;
+    a->synth = t.synth_index;
+    a->bins = t.bins;
+    a->nbq = t.nbins_q;
+    a->fflags = (t.synth ? 1 : 0) | (t.nbins_q > 0 ? 2 : 0);
+    for (int k = 0; k < t.nbins_q; ++k) a->bin_pos[k] = t.bin_pos[k];
+    if (t.nbins_q > 0) {  // register-index part of the bin for the last segment's mapping
+        const TSeg& S = t.segs.back();
+        for (int r = 0; r < TILE_NREG; ++r) {
+            uint64_t x = 0;
+            for (int j = 0; j < TILE_R; ++j)
+                if ((r >> j) & 1) x |= 1ull << t.wpos[S.rbits[j]];
+            uint32_t b = 0;
+            for (int k = 0; k < t.nbins_q; ++k) b = (b << 1) | (uint32_t)((x >> t.bin_pos[k]) & 1u);
+            a->regbin[r] = (uint16_t)b;
+        }
+    }
     a->nseg = (int)t.segs.size();
     a->nops = (int)t.ops.size();
     uint64_t wmask = 0;
@@ -486,9 +502,11 @@ cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, Tile
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = std::min<uint64_t>(a->ntiles, (uint64_t)sms * TILE_MINBLOCKS);
     std::string jerr;
-    void* jf = tile_jit_function<R>(*a, blob.data() + a->lay.mats, &jerr, nullptr);
-    if (jf) {
-        e = tile_jit_launch(jf, a, (unsigned)grid, smem, st);
+    const JitKernel* jk = tile_jit_kernel<R>(*a, blob.empty() ? nullptr : blob.data(), &jerr, nullptr);
+    if (jk) {
+        tile_jit_fill<R>(*jk, a, blob.data());
+        const uint64_t jgrid = std::min<uint64_t>(a->ntiles, (uint64_t)sms * jk->blocks);
+        e = tile_jit_launch(jk->f, a, (unsigned)jgrid, smem + jk->smem_extra, st);
     } else {
         static bool warned = false;
         if (!warned && getenv("QJ_DEBUG_JIT")) fprintf(stderr, "[qj jit] interpreter fallback: %s\n", jerr.c_str());
@@ -527,7 +545,13 @@ cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     out.grid = (unsigned)std::min<uint64_t>(a->ntiles, (uint64_t)sms * TILE_MINBLOCKS);
     std::string jerr;
-    out.jit = tile_jit_function<R>(*a, blob.empty() ? nullptr : blob.data() + a->lay.mats, &jerr, nullptr);
+    const JitKernel* jk = tile_jit_kernel<R>(*a, blob.empty() ? nullptr : blob.data(), &jerr, nullptr);
+    out.jit = jk ? jk->f : nullptr;
+    if (jk) {
+        tile_jit_fill<R>(*jk, a, blob.data());
+        out.smem += jk->smem_extra;
+        out.grid = (unsigned)std::min<uint64_t>(a->ntiles, (uint64_t)sms * jk->blocks);
+    }
     out.args.assign(reinterpret_cast<unsigned char*>(a), reinterpret_cast<unsigned char*>(a) + sizeof(TileArgs<R>));
     return cudaSuccess;
 }

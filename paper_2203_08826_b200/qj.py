@@ -36,7 +36,8 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_get_counters", "qj_state_info", "qj_last_error", "qj_version",
            "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
            "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit", "qj_collapse",
-           "qj_sample_distribution", "qj_sample", "qj_measure", "qj_state_init_host"]
+           "qj_sample_distribution", "qj_sample", "qj_measure", "qj_state_init_host",
+           "qj_simulate"]
 
 
 class QJError(RuntimeError):
@@ -123,6 +124,7 @@ def lib():
                              I, IP, IP], S),
         "qj_collapse": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_double)], S),
         "qj_state_init_host": ([ctypes.POINTER(P), P, I, I, I, U64, P], S),
+        "qj_simulate": ([P, U64, ctypes.POINTER(qj_gate), I, ctypes.c_uint32, IP, I, P], S),
         "qj_sample_distribution": ([P, I, U64, U64, ctypes.POINTER(qj_sample_opts), P, P, P], S),
         "qj_sample": ([P, IP, I, U64, U64, ctypes.POINTER(qj_sample_opts), P, P], S),
         "qj_measure": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double)], S),
@@ -474,6 +476,22 @@ class State:
         flags = (QJ_FUSE if fuse else 0) | (QJ_FUSE_GATES if fuse_gates else 0)
         _check(lib().qj_apply_circuit(self._h, arr, ng, flags))
         del keep
+
+    def simulate(self, basis, gates=None, qubits=(), fuse=True, fuse_gates=False, packed=None, out=None):
+        """reset(basis) + apply_circuit + probabilities(qubits) in one call
+        (qj_simulate: the step's ends fuse into the first / last tile pass).
+        Returns the marginal tensor (or None when qubits is empty)."""
+        import torch
+
+        arr, ng, keep = packed if packed is not None else self.pack_circuit(gates)
+        q, nq = _ints(qubits)
+        if nq and out is None:
+            out = torch.empty(1 << nq, dtype=self.real_dtype, device=self.device)
+        flags = (QJ_FUSE if fuse else 0) | (QJ_FUSE_GATES if fuse_gates else 0)
+        _check(lib().qj_simulate(self._h, ctypes.c_uint64(int(basis)), arr, ng, flags, q, nq,
+                                 ctypes.c_void_p(out.data_ptr()) if nq else None))
+        del keep
+        return out if nq else None
 
     # -- readout -----------------------------------------------------------
     def probabilities(self, qubits=None, out=None):

@@ -633,3 +633,93 @@ def test_fused_sharded_vs_oracle(dt, mode, nshards, name):
     check_close(got, exp, dt)
     assert np.max(np.abs(pf - oracle.probabilities(exp, n, [0, 1, n - 1]))) < TOL[dt]
     assert ctr["passes"] < len(circ.gates) * nshards / 2, ctr  # actually fused
+
+
+# ------------------------------------------------ many tiles per CTA (prefetch ring)
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+def test_fused_many_tiles_per_block(dt):
+    """n = 22: 1024 tiles per pass > the grid (SMs x blocks), so every CTA
+    loops over several tiles and the cp.async prefetch ring carries data
+    between iterations (at n <= 20 each CTA sees at most one tile)."""
+    n = 22
+    circ = C.random_circuit(n, 160, 22, max_targets=2, max_controls=1)
+    circ.gates += C.qft(n).gates
+    rng = np.random.default_rng(2222)
+    psi = rand_state(n, rng, dt)
+    x = to_gpu(psi, dt)
+    st = qjp.State(x, basis=None)
+    st.apply_circuit(circ.gates, fuse=True)
+    st.canonicalize()
+    st.sync()
+    check_close(x.cpu().numpy(), oracle_circuit(circ, psi, dt), dt)
+
+
+@pytest.mark.parametrize("n", [24, 26])
+def test_qft_large_closed_form_fused(n):
+    """QFT|x> closed form at 4096 / 16384 tiles per pass (c128)."""
+    x = (0x2D5A3C9 * n) & ((1 << n) - 1)
+    t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(t, basis=x)
+    st.apply_circuit(C.qft(n).gates, fuse=True)
+    st.canonicalize()
+    st.sync()
+    rng = np.random.default_rng(n)
+    idx = np.unique(np.concatenate([rng.integers(0, 2**n, 20000), [0, 2**n - 1]])).astype(np.int64)
+    got = t[torch.from_numpy(idx).cuda()].cpu().numpy()
+    m = (np.uint64(x) * idx.astype(np.uint64)) % np.uint64(2**n)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * m.astype(np.float64) / 2**n)
+    assert np.max(np.abs(got - exp)) < 1e-12
+
+
+# ------------------------------------------------ qj_simulate (fused step ends)
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("name", ["qft22", "random22", "qft12", "variational16"])
+def test_simulate_matches_separate_calls(dt, name):
+    """qj_simulate == reset + apply_circuit + probabilities: the first tile
+    pass synthesises |basis>, the last one accumulates the marginal (n >= 14);
+    small states take the SMEM program path.  Repeated calls replay a graph."""
+    n = int("".join(c for c in name if c.isdigit()))
+    circ = {"qft": lambda: C.qft(n), "random": lambda: C.random_circuit(n, 200, 5, max_targets=2, max_controls=1),
+            "variational": lambda: C.variational(n, layers=2)}[name.rstrip("0123456789")]()
+    basis = (0x9E3779B97F4A7C15 >> (64 - n)) if n < 64 else 5
+    qubits = [0, 3, n - 1, n // 2]
+    tdt = TDT[dt]
+    stream = torch.cuda.Stream()
+    ref = torch.empty(2**n, dtype=tdt, device="cuda")
+    sr = qjp.State(ref, basis=basis, stream=stream)
+    sr.apply_circuit(circ.gates, fuse=True)
+    pr = sr.probabilities(qubits)
+    sr.canonicalize()
+    sr.sync()
+    x = torch.empty(2**n, dtype=tdt, device="cuda")
+    st = qjp.State(x, basis=None, stream=stream)
+    packed = st.pack_circuit(circ.gates)
+    for rep in range(3):
+        x.fill_(float("nan"))  # the synthesised first pass must not read the buffer
+        p = st.simulate(basis, qubits=qubits, packed=packed)
+        st.canonicalize()
+        st.sync()
+        tol = TOL[dt]
+        assert np.max(np.abs(x.cpu().numpy().astype(np.complex128) - ref.cpu().numpy())) <= tol, rep
+        assert np.max(np.abs(p.cpu().numpy() - pr.cpu().numpy())) <= tol, rep
+    psi0 = np.zeros(2**n, dtype=dt)
+    psi0[basis] = 1
+    exp = oracle_circuit(circ, psi0, dt)
+    check_close(x.cpu().numpy(), exp, dt)
+
+
+def test_simulate_fallbacks_and_no_readout():
+    n = 15
+    circ = C.qft(n)
+    t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(t, basis=None)
+    assert st.simulate(7, circ.gates, qubits=()) is None  # nq = 0
+    st.canonicalize()
+    st.sync()
+    y = np.arange(2**n, dtype=np.uint64)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * ((7 * y) % 2**n).astype(np.float64) / 2**n)
+    assert np.max(np.abs(t.cpu().numpy() - exp)) < 1e-12
+    p = st.simulate(7, circ.gates, qubits=list(range(11)), fuse=True)  # nq > 10: three-call path
+    assert abs(float(p.sum()) - 1) < 1e-12
+    p = st.simulate(7, circ.gates, qubits=[0, 1], fuse=False)  # unfused: three-call path
+    assert abs(float(p.sum()) - 1) < 1e-12
