@@ -372,22 +372,42 @@ __device__ __forceinline__ uint32_t thread_loc(const TileArgs<R>& a, int s, int 
 // ---------------------------------------------------------------- tile phases
 // Per-tile base index (non-window bits of `tile`) and the per-tile products of
 // the tile-dependent phase terms (slots) into SMEM.
+// Slot products of one tile: warp w fills slots w, w + warps, ...; its lanes
+// take every 32nd term of the slot (independent loads, no dependent chain) and
+// a fixed xor-butterfly multiplies the 32 partial products, so the result is
+// deterministic and the same in every kernel flavour.
+template <typename R>
+__device__ __forceinline__ void tile_slots(const TileArgs<R>& a, uint64_t tg, Cx<R>* tab, int tid) {
+    const TSlot* slots = reinterpret_cast<const TSlot*>(a.tables + a.lay.slots);
+    const TTerm<R>* terms = reinterpret_cast<const TTerm<R>*>(a.tables + a.lay.terms);
+    const int lane = tid & 31;
+    for (int e = tid >> 5; e < a.nslots; e += TILE_THREADS / 32) {
+        const TSlot sl = slots[e];
+        Cx<R> p = cone<R>();
+        for (uint32_t t = sl.t0 + lane; t < sl.t1; t += 32)
+            if ((tg & terms[t].cmask) == terms[t].cval) p = cmul(p, terms[t].f);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) p = cmul(p, shfl_xor(p, o));
+        if (lane == 0) tab[e] = p;
+    }
+}
+
 template <typename R>
 __device__ __forceinline__ uint64_t tile_begin(const TileArgs<R>& a, uint64_t tile, Cx<R>* tab, int tid) {
     uint64_t tb = tile;
 #pragma unroll
     for (int i = 0; i < TILE_W; ++i) tb = insert_zero(tb, a.wpos[i]);
-    const TSlot* slots = reinterpret_cast<const TSlot*>(a.tables + a.lay.slots);
-    const TTerm<R>* terms = reinterpret_cast<const TTerm<R>*>(a.tables + a.lay.terms);
-    const uint64_t tg = tb | a.gbase;  // predicates see the global bits too
-    for (int e = tid; e < a.nslots; e += TILE_THREADS) {
-        Cx<R> p = cone<R>();
-        const TSlot sl = slots[e];
-        for (uint32_t t = sl.t0; t < sl.t1; ++t)
-            if ((tg & terms[t].cmask) == terms[t].cval) p = cmul(p, terms[t].f);
-        tab[e] = p;
-    }
+    tile_slots(a, tb | a.gbase, tab, tid);  // predicates see the global bits too
     return tb;
+}
+
+// JIT kernels address the tile with compile-time register offsets: one
+// amplitude copy / store at element offset `off` from a per-thread base.
+template <typename R>
+__device__ __forceinline__ void cp_amp(Cx<R>* s, const Cx<R>* g);
+template <typename R>
+__device__ __forceinline__ void st_amp(Cx<R>* g, Cx<R> v) {
+    store_amp(g, 0, v);
 }
 
 // HBM <-> registers with the mapping of segment s (s = 0 loads, s = last stores).
@@ -474,6 +494,15 @@ __device__ __forceinline__ void tile_prefetch_issue(const TileArgs<R>& a, uint64
         if constexpr (sizeof(R) == 8) cp_async16(sm + y, psi + x);
         else cp_async8(sm + y, psi + x);
     }
+}
+
+template <>
+__device__ __forceinline__ void cp_amp<double>(Cx<double>* s, const Cx<double>* g) {
+    cp_async16(s, g);
+}
+template <>
+__device__ __forceinline__ void cp_amp<float>(Cx<float>* s, const Cx<float>* g) {
+    cp_async8(s, g);
 }
 
 template <typename R>

@@ -254,7 +254,11 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
         return;
     }
     std::vector<int>& phys = *ctx.phys;
-    const int C = ctx.amp_bytes == 16 ? 3 : 4;  // 128-byte runs: 8 x c128 / 16 x c64
+    int C = ctx.amp_bytes == 16 ? 3 : 4;  // 128-byte runs: 8 x c128 / 16 x c64
+    if (const char* e = getenv("QJ_TILE_C")) {  // experiment: wider contiguous runs
+        const int c = atoi(e);
+        if (c >= 2 && c <= 6) C = c;
+    }
     const uint64_t low = (1ull << C) - 1ull;
     const int max_terms = TILE_MAXTERMS;
     PassBuild pb;
