@@ -70,7 +70,7 @@ struct TileSpec {
 // Pinned-host + device ring for the per-pass program buffers.
 struct TileStaging {
     static constexpr int kSlots = 8;
-    static constexpr size_t kBytes = 256 * 1024;
+    static constexpr size_t kBytes = 512 * 1024;
     unsigned char* host = nullptr;  // pinned, kSlots * kBytes
     unsigned char* dev = nullptr;   // device, kSlots * kBytes
     cudaEvent_t ev[kSlots] = {};

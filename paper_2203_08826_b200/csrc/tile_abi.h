@@ -11,14 +11,17 @@ namespace qj {
 #ifndef QJ_TILE_R
 #define QJ_TILE_R 4
 #endif
-constexpr int TILE_W = 12;
+#ifndef QJ_TILE_W
+#define QJ_TILE_W 13
+#endif
+constexpr int TILE_W = QJ_TILE_W;            // window bits: a tile is 2^TILE_W amplitudes
 constexpr int TILE_R = QJ_TILE_R;          // register bits per thread (3 or 4)
 constexpr int TILE_T = TILE_W - TILE_R;    // thread-index bits
 constexpr int TILE_THREADS = 1 << TILE_T;
 constexpr int TILE_NREG = 1 << TILE_R;
 constexpr int TILE_TCH = (TILE_T + 3) / 4;  // 4-bit chunks of the thread index
 #ifndef QJ_TILE_MINBLOCKS
-#define QJ_TILE_MINBLOCKS 2
+#define QJ_TILE_MINBLOCKS 1
 #endif
 constexpr int TILE_MINBLOCKS = QJ_TILE_MINBLOCKS;  // resident CTAs per SM (JIT kernels: per-launch option)
 constexpr int TILE_MAXSEG = 8;
@@ -51,6 +54,8 @@ struct TOp {
 struct TSeg {
     int8_t tbits[TILE_T];  // window-bit index mapped to thread-id bit i
     int8_t rbits[TILE_R];  // window-bit index mapped to register-index bit j
+    int8_t split;          // thread-id bit that holds the same window bit in this and the
+                           // previous segment (half-buffer transposes), -1 = none
     uint16_t op0, op1;     // op range
 };
 

@@ -19,11 +19,11 @@ template <typename R>
 __host__ __device__ __forceinline__ uint32_t swz(uint32_t i);
 template <>
 __host__ __device__ __forceinline__ uint32_t swz<double>(uint32_t i) {
-    return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7u);
+    return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9) ^ (i >> 12)) & 7u);
 }
 template <>
 __host__ __device__ __forceinline__ uint32_t swz<float>(uint32_t i) {
-    return i ^ (((i >> 4) ^ (i >> 8)) & 15u);
+    return i ^ (((i >> 4) ^ (i >> 8) ^ (i >> 12)) & 15u);
 }
 
 template <typename R>
@@ -382,6 +382,28 @@ __device__ __forceinline__ void tile_slots(const TileArgs<R>& a, uint64_t tg, Cx
     const TTerm<R>* terms = reinterpret_cast<const TTerm<R>*>(a.tables + a.lay.terms);
     const int lane = tid & 31;
     for (int e = tid >> 5; e < a.nslots; e += TILE_THREADS / 32) {
+        const TSlot sl = slots[e];
+        Cx<R> p = cone<R>();
+        for (uint32_t t = sl.t0 + lane; t < sl.t1; t += 32)
+            if ((tg & terms[t].cmask) == terms[t].cval) p = cmul(p, terms[t].f);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) p = cmul(p, shfl_xor(p, o));
+        if (lane == 0) tab[e] = p;
+    }
+}
+
+// JIT kernels stage the slot terms (predicate + factor) and slot ranges in
+// shared memory once per CTA, so the per-tile products read no global memory.
+template <typename R>
+struct STerm {
+    uint64_t cmask, cval;
+    Cx<R> f;
+};
+template <typename R>
+__device__ __forceinline__ void tile_slots_staged(const STerm<R>* terms, const TSlot* slots, int nslots, uint64_t tg,
+                                                  Cx<R>* tab, int tid) {
+    const int lane = tid & 31;
+    for (int e = tid >> 5; e < nslots; e += TILE_THREADS / 32) {
         const TSlot sl = slots[e];
         Cx<R> p = cone<R>();
         for (uint32_t t = sl.t0 + lane; t < sl.t1; t += 32)

@@ -17,6 +17,10 @@
 
 namespace qj {
 
+// the JIT kernels take TileArgs by value through cuLaunchKernel (4 KiB..32 KiB parameter space)
+static_assert(sizeof(TileArgs<double>) <= 32764 && sizeof(TileArgs<float>) <= 32764, "TileArgs exceeds the kernel parameter limit");
+
+
 // ======================================================================
 // Staging ring
 // ======================================================================

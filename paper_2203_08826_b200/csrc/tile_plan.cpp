@@ -135,10 +135,10 @@ bool make_op(const LGate& g, const std::vector<int>& phys, HOp& op) {
     }
 }
 
-// Choose the thread-bit order of a segment: lanes 0..C-1 on window bits of
-// distinct residues mod C (conflict-free swizzled SMEM), low bits first when
-// the segment touches HBM.
-void thread_bits(uint32_t rsel, int C, bool global, int8_t* tb) {
+// Choose the thread-bit order of a segment: lanes 0..M-1 on window bits of
+// distinct residues mod M (the swizzle period: conflict-free SMEM), or the C
+// low bits first when the segment touches HBM.
+void thread_bits(uint32_t rsel, int C, int M, bool global, int8_t* tb) {
     std::vector<int> avail;
     for (int j = 0; j < TILE_W; ++j)
         if (!((rsel >> j) & 1)) avail.push_back(j);
@@ -150,9 +150,9 @@ void thread_bits(uint32_t rsel, int C, bool global, int8_t* tb) {
     if (global) {
         for (int j = 0; j < C; ++j) take(j);  // low window bits on lanes 0..C-1
     } else {
-        for (int res = 0; res < C; ++res) {
+        for (int res = 0; res < M; ++res) {
             for (int j : avail)
-                if (j % C == res) {
+                if (j % M == res) {
                     take(j);
                     break;
                 }
@@ -165,7 +165,11 @@ void thread_bits(uint32_t rsel, int C, bool global, int8_t* tb) {
 }  // namespace
 
 // Build the TileSpec of one pass.
-static bool build_tile(const PassBuild& pb, int nl, int C, TileSpec& ts) {
+// carried (optional): diagonal items whose terms are all still pending at the
+// end of the pass and touch a bit outside the window are left out of the pass
+// and returned, so the caller can move them to the front of the next pass
+// (they commute with everything in between).
+static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, std::vector<int>* carried = nullptr) {
     // window: pad to TILE_W bits with the highest unused local bits
     uint64_t W = pb.W;
     for (int b = nl - 1; b >= 0 && popc(W) < TILE_W; --b) W |= 1ull << b;
@@ -187,20 +191,34 @@ static bool build_tile(const PassBuild& pb, int nl, int C, TileSpec& ts) {
     };
     std::vector<SegB> segs(1);
     std::vector<HTerm> pending;
+    std::vector<int> pend_src;                    // item of each pending term
+    std::vector<char> touched(pb.items.size(), 0);  // an item's term went into a run
+    std::vector<char> skip(pb.items.size(), 0);     // carried items (final flush only)
     auto flush = [&](uint64_t conflict_mask, bool all) {
         HOp run;
         run.type = TO_RUN;
         std::vector<HTerm> keep;
-        for (auto& t : pending) {
-            if (all || (t.mask & conflict_mask)) run.terms.push_back(t);
-            else keep.push_back(t);
+        std::vector<int> keep_src;
+        for (size_t i = 0; i < pending.size(); ++i) {
+            const HTerm& t = pending[i];
+            if (skip[pend_src[i]]) continue;
+            if (all || (t.mask & conflict_mask)) {
+                run.terms.push_back(t);
+                touched[pend_src[i]] = 1;
+            } else {
+                keep.push_back(t);
+                keep_src.push_back(pend_src[i]);
+            }
         }
         pending.swap(keep);
+        pend_src.swap(keep_src);
         if (!run.terms.empty()) segs.back().ops.push_back(std::move(run));
     };
-    for (const Item& it : pb.items) {
+    for (size_t ii = 0; ii < pb.items.size(); ++ii) {
+        const Item& it = pb.items[ii];
         if (it.diag) {
             pending.insert(pending.end(), it.terms.begin(), it.terms.end());
+            pend_src.insert(pend_src.end(), it.terms.size(), (int)ii);
             continue;
         }
         uint32_t tsel = 0;
@@ -219,6 +237,19 @@ static bool build_tile(const PassBuild& pb, int nl, int C, TileSpec& ts) {
         }
         flush(it.tmask, false);
         segs.back().ops.push_back(it.op);
+    }
+    if (carried) {
+        carried->clear();
+        for (size_t ii = 0; ii < pb.items.size(); ++ii) {
+            const Item& it = pb.items[ii];
+            if (!it.diag || touched[ii]) continue;
+            bool out = false;
+            for (const HTerm& t : it.terms) out |= (t.mask & ~W) != 0;
+            if (out) {
+                skip[ii] = 1;
+                carried->push_back((int)ii);
+            }
+        }
     }
     flush(0, true);
     // the first and last segments touch HBM: their register bits must avoid the low bits
@@ -239,11 +270,39 @@ static bool build_tile(const PassBuild& pb, int nl, int C, TileSpec& ts) {
         const bool global = (s == 0 || s + 1 == segs.size());
         for (int j = 0, k = 0; j < TILE_W; ++j)
             if ((segs[s].rsel >> j) & 1) S.rbits[k++] = (int8_t)j;
-        thread_bits(segs[s].rsel, C, global, S.tbits);
+        thread_bits(segs[s].rsel, C, M, global, S.tbits);
         S.op0 = (uint16_t)ts.ops.size();
         for (auto& op : segs[s].ops) ts.ops.push_back(op);
         S.op1 = (uint16_t)ts.ops.size();
+        S.split = -1;
         ts.segs.push_back(S);
+    }
+    // Half-buffer transposes: the move into segment s can run
+    // in two rounds through a buffer of 2^(W-1) amplitudes when one window bit
+    // b sits at the same thread-id position p in both layouts -- round k is
+    // done by the threads with tid bit p = k, which write and then read only
+    // amplitudes with x_b = k.  b must lie above the swizzled low bits so the
+    // compressed SMEM index keeps the bank mapping.  Segment s's order may be
+    // permuted among its unconstrained positions (>= the lane constraint) to
+    // line b up; segment s-1 is never touched, so earlier choices stay valid.
+    for (size_t s = 1; s < ts.segs.size(); ++s) {
+        TSeg& P = ts.segs[s - 1];
+        TSeg& S = ts.segs[s];
+        const int lim = (s + 1 == ts.segs.size()) ? C : M;  // positions below are pinned
+        int best = -1, bestq = -1;
+        for (int p = TILE_T - 1; p >= 0 && best < 0; --p) {
+            const int b = P.tbits[p];
+            if (b < M) continue;  // swz<R> mixes the bits below M
+            for (int q = 0; q < TILE_T; ++q)
+                if (S.tbits[q] == b && (q == p || (q >= lim && p >= lim))) {
+                    best = p;
+                    bestq = q;
+                    break;
+                }
+        }
+        if (best < 0) continue;
+        std::swap(S.tbits[best], S.tbits[bestq]);
+        S.split = (int8_t)best;
     }
     return (int)ts.ops.size() <= TILE_MAXOPS;
 }
@@ -254,7 +313,10 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
         return;
     }
     std::vector<int>& phys = *ctx.phys;
-    int C = ctx.amp_bytes == 16 ? 3 : 4;  // 128-byte runs: 8 x c128 / 16 x c64
+    // 256-byte contiguous HBM runs (16 x c128 / 32 x c64): 128-byte runs cap a
+    // pass with high window bits at ~0.66 of the HBM peak (tools/membench.cu)
+    int C = ctx.amp_bytes == 16 ? 4 : 5;
+    const int M = ctx.amp_bytes == 16 ? 3 : 4;  // swizzle period (swz<R>): lanes of one SMEM wavefront
     if (const char* e = getenv("QJ_TILE_C")) {  // experiment: wider contiguous runs
         const int c = atoi(e);
         if (c >= 2 && c <= 6) C = c;
@@ -263,8 +325,12 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
     const int max_terms = TILE_MAXTERMS;
     PassBuild pb;
     pb.W = low;
-    auto close = [&]() {
+    // allow_carry: another pass follows, so diagonal terms still pending at the
+    // end of this one may start it instead (build_tile)
+    auto close = [&](bool allow_carry) {
         if (pb.items.empty()) return;
+        PassBuild next;
+        next.W = low;
         if (pb.singles.size() == 1) {
             // a single gate: the specialised single-gate pass touches fewer bytes
             for (const Step& st : pb.singles[0]) out.push_back(st);
@@ -272,7 +338,18 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
             Step s;
             s.type = Step::TILE;
             s.shard = 0;
-            if (build_tile(pb, ctx.nl, C, s.tile) && tile_fits(s.tile, ctx.nl, ctx.amp_bytes)) {
+            std::vector<int> carried;
+            bool has_op = false;
+            for (const Item& it : pb.items) has_op |= !it.diag;
+            const bool carry = allow_carry && has_op && !(getenv("QJ_TILE_CARRY") && getenv("QJ_TILE_CARRY")[0] == '0');
+            if (build_tile(pb, ctx.nl, C, M, s.tile, carry ? &carried : nullptr) &&
+                tile_fits(s.tile, ctx.nl, ctx.amp_bytes)) {
+                for (int i : carried) {
+                    next.nterms += (int)pb.items[i].terms.size();
+                    next.cost += 0.05 * (double)pb.items[i].terms.size();
+                    next.items.push_back(std::move(pb.items[i]));
+                    next.singles.push_back(std::move(pb.singles[i]));
+                }
                 s.alg_bytes = 2.0 * ctx.amp_bytes * std::ldexp(1.0, ctx.nl);
                 if (getenv("QJ_DEBUG_PLAN")) {
                     int nruns = 0, nterms = 0;
@@ -285,6 +362,14 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
                     for (int j = 0; j < TILE_W; ++j) fprintf(stderr, " %d", s.tile.wpos[j]);
                     fprintf(stderr, " | %zu segs, %zu ops, %d runs, %d terms\n", s.tile.segs.size(),
                             s.tile.ops.size(), nruns, nterms);
+                    if (getenv("QJ_DEBUG_PLAN")[0] == '2')
+                        for (const TSeg& S : s.tile.segs) {
+                            fprintf(stderr, "    seg r:");
+                            for (int j = 0; j < TILE_R; ++j) fprintf(stderr, " %d", S.rbits[j]);
+                            fprintf(stderr, " t:");
+                            for (int j = 0; j < TILE_T; ++j) fprintf(stderr, " %d", S.tbits[j]);
+                            fprintf(stderr, " split %d\n", S.split);
+                        }
                 }
                 // one pass per shard: the same program, the shard's global bits
                 // enter the predicates through gbase (tile.h)
@@ -300,8 +385,7 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
                     for (const Step& st : v) out.push_back(st);
             }
         }
-        pb = PassBuild();
-        pb.W = low;
+        pb = std::move(next);
     };
     auto single = [&](const LGate& g) {
         std::vector<Step> v;
@@ -406,9 +490,10 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
             pb.items.push_back(std::move(it));
             pb.singles.push_back(single(g));
         }
-        close();
+        close(!deferred.empty());
         remaining.swap(deferred);
     }
+    close(false);  // terms carried out of the last pass
 }
 
 }  // namespace qj

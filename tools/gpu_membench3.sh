@@ -1,0 +1,6 @@
+#!/bin/bash
+out=gpurun_out/membench3.jsonl; : > $out
+for cfg in "3 21" "3 12" "4 22"; do for B in 1 2; do for pm in 0 1 2; do
+  timeout 60 ./tools/membench 30 $cfg $B c 5 $pm >> $out
+done; done; done
+echo done

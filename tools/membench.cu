@@ -62,6 +62,43 @@ __global__ void __launch_bounds__(256, MINB) tile_copy(Args a) {
     }
 }
 
+// Cluster pairs: the two CTAs of a cluster take sibling tiles (differing in the
+// lowest tile bit, i.e. adjacent 128-byte chunks) and meet at a cluster barrier
+// before each tile's loads, so DRAM sees both halves of every 256-byte run together.
+template <int MINB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, MINB) tile_copy_pair(Args a) {
+    const int tid = threadIdx.x;
+    unsigned rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint64_t pairs = a.ntiles / 2, npair_grid = gridDim.x / 2, pid = blockIdx.x / 2;
+    const int H = 12 - a.L;
+    for (uint64_t pr = pid; pr < pairs; pr += npair_grid) {
+        const uint64_t tile = 2 * pr + rank;
+        uint64_t tb = tile;
+        for (int i = 0; i < a.L; ++i) tb = insert_zero(tb, i);
+        for (int i = 0; i < H; ++i) tb = insert_zero(tb, a.P + i);
+        if (a.group) {
+            asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+        }
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint32_t w = (uint32_t)tid | ((uint32_t)r << 8);
+            const uint64_t lo = w & ((1u << a.L) - 1), hi = w >> a.L;
+            v[r] = __ldcg(a.psi + (tb | lo | (hi << a.P)));
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint32_t w = (uint32_t)tid | ((uint32_t)r << 8);
+            const uint64_t lo = w & ((1u << a.L) - 1), hi = w >> a.L;
+            double2 y = v[r];
+            asm volatile("" : "+d"(y.x), "+d"(y.y));
+            __stcg(a.psi + (tb | lo | (hi << a.P)), y);
+        }
+    }
+}
+
 int main(int argc, char** argv) {
     const int n = argc > 1 ? atoi(argv[1]) : 30;
     const int L = argc > 2 ? atoi(argv[2]) : 3;
@@ -80,7 +117,14 @@ int main(int argc, char** argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const unsigned grid = sms * B;
+    const int pairmode = argc > 7 ? atoi(argv[7]) : 0;  // 1: cluster pairs, 2: cluster pairs + barrier
+    a.group = pairmode == 2;
     auto launch = [&]() {
+        if (pairmode) {
+            if (B == 1) tile_copy_pair<1><<<grid, 256>>>(a);
+            else tile_copy_pair<2><<<grid, 256>>>(a);
+            return;
+        }
         switch (B) {
             case 1: tile_copy<1><<<grid, 256>>>(a); break;
             case 2: tile_copy<2><<<grid, 256>>>(a); break;
@@ -105,7 +149,7 @@ int main(int argc, char** argv) {
     }
     const cudaError_t err = cudaGetLastError();
     const double gbs = 2.0 * bytes / (sum / reps * 1e-3) / 1e9;
-    printf("{\"n\": %d, \"L\": %d, \"P\": %d, \"blocks\": %d, \"order\": \"%s\", \"ms\": %.3f, \"best_ms\": %.3f, \"GBps\": %.1f, \"err\": \"%s\"}\n",
-           n, L, P, B, blocked ? "b" : "c", sum / reps, best, gbs, cudaGetErrorString(err));
+    printf("{\"pair\": %d, \"n\": %d, \"L\": %d, \"P\": %d, \"blocks\": %d, \"order\": \"%s\", \"ms\": %.3f, \"best_ms\": %.3f, \"GBps\": %.1f, \"err\": \"%s\"}\n",
+           pairmode, n, L, P, B, blocked ? "b" : "c", sum / reps, best, gbs, cudaGetErrorString(err));
     return 0;
 }
