@@ -12,7 +12,7 @@ namespace qj {
 #define QJ_TILE_R 4
 #endif
 #ifndef QJ_TILE_W
-#define QJ_TILE_W 13
+#define QJ_TILE_W 12
 #endif
 constexpr int TILE_W = QJ_TILE_W;            // window bits: a tile is 2^TILE_W amplitudes
 constexpr int TILE_R = QJ_TILE_R;          // register bits per thread (3 or 4)
@@ -21,7 +21,7 @@ constexpr int TILE_THREADS = 1 << TILE_T;
 constexpr int TILE_NREG = 1 << TILE_R;
 constexpr int TILE_TCH = (TILE_T + 3) / 4;  // 4-bit chunks of the thread index
 #ifndef QJ_TILE_MINBLOCKS
-#define QJ_TILE_MINBLOCKS 1
+#define QJ_TILE_MINBLOCKS (QJ_TILE_W >= 13 ? 1 : 2)
 #endif
 constexpr int TILE_MINBLOCKS = QJ_TILE_MINBLOCKS;  // resident CTAs per SM (JIT kernels: per-launch option)
 constexpr int TILE_MAXSEG = 8;

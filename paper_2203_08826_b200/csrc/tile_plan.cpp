@@ -285,7 +285,8 @@ static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, 
     // compressed SMEM index keeps the bank mapping.  Segment s's order may be
     // permuted among its unconstrained positions (>= the lane constraint) to
     // line b up; segment s-1 is never touched, so earlier choices stay valid.
-    for (size_t s = 1; s < ts.segs.size(); ++s) {
+    const char* pipe = getenv("QJ_TILE_PIPE");  // only the pipelined JIT form uses splits
+    for (size_t s = 1; s < ts.segs.size() && pipe && pipe[0] == '1'; ++s) {
         TSeg& P = ts.segs[s - 1];
         TSeg& S = ts.segs[s];
         const int lim = (s + 1 == ts.segs.size()) ? C : M;  // positions below are pinned
@@ -315,7 +316,9 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
     std::vector<int>& phys = *ctx.phys;
     // 256-byte contiguous HBM runs (16 x c128 / 32 x c64): 128-byte runs cap a
     // pass with high window bits at ~0.66 of the HBM peak (tools/membench.cu)
-    int C = ctx.amp_bytes == 16 ? 4 : 5;
+    // with a 13-bit window; with 12 bits the window holds one fewer high bit
+    // and 128-byte runs keep QFT30 at three passes
+    int C = (ctx.amp_bytes == 16 ? 3 : 4) + (TILE_W >= 13 ? 1 : 0);
     const int M = ctx.amp_bytes == 16 ? 3 : 4;  // swizzle period (swz<R>): lanes of one SMEM wavefront
     if (const char* e = getenv("QJ_TILE_C")) {  // experiment: wider contiguous runs
         const int c = atoi(e);
