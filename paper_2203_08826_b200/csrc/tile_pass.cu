@@ -228,6 +228,22 @@ bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned 
                 groups.push_back({best, g});
                 rest.swap(keep);
             }
+            // slot terms on an anchor bit (the anchor plus at most one C bit) join that
+            // anchored run: its per-tile slot factor folds into the run's scalar
+            // instead of a second multiply of the same registers
+            if (!groups.empty()) {
+                std::vector<const HTerm*> keep;
+                for (auto* ht : slotable) {
+                    const uint64_t wb = ht->mask & wmask;
+                    int gi = -1;
+                    if (wb && popc64(wb) == 1 && popc64(ht->mask) <= 2)
+                        for (size_t q = 0; q < groups.size(); ++q)
+                            if (wb == (1ull << groups[q].first)) gi = (int)q;
+                    if (gi >= 0) groups[gi].second.push_back(ht);
+                    else keep.push_back(ht);
+                }
+                slotable.swap(keep);
+            }
             // the rest: window-only terms with <= 1 register bit (or register-only) go to
             // host-built per-thread tables; anything else is a generic L term
             std::vector<cd> TA, TB, PT;
