@@ -114,8 +114,8 @@ struct qj_state_s {
 };
 
 static const char* kProfNames[] = {"gate_dense", "gate_x",     "gate_swap", "diag_table", "diag_phase",
-                                   "diag_neg",   "tile",       "exchange",  "small"};
-enum { PROF_TILE = 6, PROF_EXCHANGE = 7, PROF_SMALL = 8, PROF_N = 9 };
+                                   "diag_neg",   "tile",       "exchange",  "small",     "init"};
+enum { PROF_TILE = 6, PROF_EXCHANGE = 7, PROF_SMALL = 8, PROF_INIT = 9, PROF_N = 10 };
 
 namespace {
 
@@ -1419,11 +1419,18 @@ static qj_status run_sim(qj_state s, qj_state_s::CachedPlan& p) {
     cudaError_t e = cudaSuccess;
     const size_t nb = p.nq > 0 ? (size_t)1 << p.nq : 0;
     if (nb) e = cudaMemsetAsync(p.sim_bins, 0, nb * sizeof(double), s->stream);
-    if (e == cudaSuccess && p.init_first)
-        e = by_dtype(s->dt, [&](auto z) {
-            using R = decltype(z);
-            return run_init<R>(s->shards[0], s->nl, p.basis, true, s->stream, s->ls);
-        });
+    {
+        // |basis> before the circuit: written by the init kernel, or -- when the
+        // first step is a tile pass that synthesises the one tile holding the
+        // basis amplitude -- zeros here and that tile there (every other tile
+        // of |basis> is zero in and zero out)
+        ProfScope prof(s, PROF_INIT, (double)s->amp_bytes * std::ldexp(1.0, s->nl));
+        if (e == cudaSuccess)
+            e = by_dtype(s->dt, [&](auto z) {
+                using R = decltype(z);
+                return run_init<R>(s->shards[0], s->nl, p.basis, p.init_first, s->stream, s->ls);
+            });
+    }
     if (e != cudaSuccess) return cuda_fail(e, "simulate prologue");
     if (qj_status q = run_cached(s, p)) return q;
     if (nb && !p.marg_last) {
@@ -1505,7 +1512,7 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
             Step& f = p->steps.front();
             f.tile.synth = true;
             f.tile.synth_index = basis;
-            f.alg_bytes = (double)s->amp_bytes * std::ldexp(1.0, s->nl);  // writes only
+            f.alg_bytes = 2.0 * s->amp_bytes * std::ldexp(1.0, TILE_W);  // one live tile (the rest: init kernel)
         }
         if (nq > 0) {
             cudaError_t e = cudaMalloc(&p->sim_bins, sizeof(double) << nq);
