@@ -344,7 +344,9 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
             std::vector<int> carried;
             bool has_op = false;
             for (const Item& it : pb.items) has_op |= !it.diag;
-            const bool carry = allow_carry && has_op && !(getenv("QJ_TILE_CARRY") && getenv("QJ_TILE_CARRY")[0] == '0');
+            // opt-in (QJ_TILE_CARRY=1): measured slower -- the next pass's anchored runs
+            // gain per-tile factors
+            const bool carry = allow_carry && has_op && getenv("QJ_TILE_CARRY") && getenv("QJ_TILE_CARRY")[0] == '1';
             if (build_tile(pb, ctx.nl, C, M, s.tile, carry ? &carried : nullptr) &&
                 tile_fits(s.tile, ctx.nl, ctx.amp_bytes)) {
                 for (int i : carried) {
