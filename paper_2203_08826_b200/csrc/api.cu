@@ -90,7 +90,7 @@ struct qj_state_s {
         // qj_simulate plans: |basis> synthesised by the first tile pass (else an
         // init launch), the marginal fused into the last tile pass (else a
         // marginal launch), bins owned by the plan
-        bool sim = false, init_first = false, marg_last = false;
+        bool sim = false, init_first = false, marg_last = false, init_none = false;
         uint64_t basis = 0;
         int nq = 0;
         int qpos[16] = {};
@@ -1415,6 +1415,11 @@ qj_status qj_measure(qj_state s, const int* qubits, int nq, uint64_t seed, uint6
 }
 
 // ------------------------------------------------------------------ qj_simulate
+// QJ_LIVE_TILES=0 runs every later tile pass over the whole state (A/B check)
+static bool live_tiles_on() {
+    static const bool on = !(getenv("QJ_LIVE_TILES") && getenv("QJ_LIVE_TILES")[0] == '0');
+    return on;
+}
 static qj_status run_sim(qj_state s, qj_state_s::CachedPlan& p) {
     cudaError_t e = cudaSuccess;
     const size_t nb = p.nq > 0 ? (size_t)1 << p.nq : 0;
@@ -1423,13 +1428,17 @@ static qj_status run_sim(qj_state s, qj_state_s::CachedPlan& p) {
         // |basis> before the circuit: written by the init kernel, or -- when the
         // first step is a tile pass that synthesises the one tile holding the
         // basis amplitude -- zeros here and that tile there (every other tile
-        // of |basis> is zero in and zero out)
-        ProfScope prof(s, PROF_INIT, (double)s->amp_bytes * std::ldexp(1.0, s->nl));
-        if (e == cudaSuccess)
-            e = by_dtype(s->dt, [&](auto z) {
-                using R = decltype(z);
-                return run_init<R>(s->shards[0], s->nl, p.basis, p.init_first, s->stream, s->ls);
-            });
+        // of |basis> is zero in and zero out); nothing at all when a later
+        // live-tile pass writes every tile before any amplitude outside the
+        // tiles written so far is read (init_none)
+        if (!p.init_none) {
+            ProfScope prof(s, PROF_INIT, (double)s->amp_bytes * std::ldexp(1.0, s->nl));
+            if (e == cudaSuccess)
+                e = by_dtype(s->dt, [&](auto z) {
+                    using R = decltype(z);
+                    return run_init<R>(s->shards[0], s->nl, p.basis, p.init_first, s->stream, s->ls);
+                });
+        }
     }
     if (e != cudaSuccess) return cuda_fail(e, "simulate prologue");
     if (qj_status q = run_cached(s, p)) return q;
@@ -1513,6 +1522,29 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
             f.tile.synth = true;
             f.tile.synth_index = basis;
             f.alg_bytes = 2.0 * s->amp_bytes * std::ldexp(1.0, TILE_W);  // one live tile (the rest: init kernel)
+            // the run of tile passes after it: amplitudes whose bits outside
+            // every window so far differ from |basis> are still zero, and each
+            // pass maps every tile onto itself, so only the tiles whose
+            // not-yet-windowed bits equal the basis bits are live
+            const uint64_t all = s->nl >= 64 ? ~0ull : (1ull << s->nl) - 1;
+            uint64_t windowed = 0;
+            for (size_t i = 0; i < p->steps.size() && p->steps[i].type == Step::TILE && live_tiles_on(); ++i) {
+                Step& t = p->steps[i];
+                uint64_t wm = 0;
+                for (int j = 0; j < TILE_W; ++j) wm |= 1ull << t.tile.wpos[j];
+                if (i > 0) {
+                    t.tile.fix_mask = all & ~windowed & ~wm;
+                    t.tile.fix_val = basis & t.tile.fix_mask;
+                    t.tile.zero_mask = wm & ~windowed;
+                    t.tile.zero_val = basis & t.tile.zero_mask;
+                    const int f = __builtin_popcountll(t.tile.fix_mask), z = __builtin_popcountll(t.tile.zero_mask);
+                    t.alg_bytes = s->amp_bytes * (std::ldexp(1.0, s->nl - f - z) + std::ldexp(1.0, s->nl - f));
+                    // each pass reads only amplitudes the previous one wrote: once a
+                    // pass writes every tile, no amplitude is read before it is written
+                    if (!t.tile.fix_mask) p->init_none = true;
+                }
+                windowed |= wm;
+            }
         }
         if (nq > 0) {
             cudaError_t e = cudaMalloc(&p->sim_bins, sizeof(double) << nq);
@@ -1542,7 +1574,7 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
                     using R = decltype(z);
                     return tile_prepare<R>(st.tile, s->shards[0], s->nl, t);
                 });
-                if (e != cudaSuccess || ((st.tile.synth || st.tile.nbins_q) && !t.jit)) {
+                if (e != cudaSuccess || ((st.tile.synth || st.tile.nbins_q || st.tile.fix_mask || st.tile.zero_mask) && !t.jit)) {
                     tile_release(t);
                     release_plan(p);
                     return e != cudaSuccess ? cuda_fail(e, "tile prepare") : fail(QJ_ERR_CUDA, "simulate: JIT unavailable");

@@ -58,6 +58,13 @@ struct TileSpec {
     // listed physical bits (first = MSB of the bin index) into `bins`.
     bool synth = false;
     uint64_t synth_index = 0;
+    // qj_simulate, later passes of a |basis> run: bits no earlier pass has
+    // targeted still equal the basis bits (zero elsewhere), so only the tiles
+    // whose fixed bits match are live; ntiles counts those, bit-inserted
+    uint64_t fix_mask = 0, fix_val = 0;
+    // ... and of each live tile only the amplitudes whose newly windowed bits
+    // (zero_mask) equal the basis bits are nonzero: the rest load as zeros
+    uint64_t zero_mask = 0, zero_val = 0;
     int nbins_q = 0;            // 0 = no fused marginal
     int8_t bin_pos[16] = {};
     double* bins = nullptr;

@@ -124,6 +124,9 @@ struct TileArgs {
     Cx<R> uc[TILE_MAXUC];
     // qj_simulate fusions (JIT kernels; see tile.h)
     uint64_t synth;          // local index of the basis amplitude (synthesised first pass)
+    uint64_t fixval;         // live-tile passes: value of the fixed bits (fixmask), OR-ed into every tile base
+    uint64_t fixmask;        // live-tile passes: physical bits still equal to the basis bits (0 = all tiles)
+    uint64_t zmask, zval;    // live-tile passes: window bits first windowed here; amplitudes off zval are zero (not read)
     double* bins;            // fused marginal: 2^nbq fp64 bins (global)
     int nbq, fflags;         // fflags: 1 = synthesise the first load, 2 = fused marginal
     int8_t bin_pos[16];      // physical bit of output bit k (k = 0 is the MSB)

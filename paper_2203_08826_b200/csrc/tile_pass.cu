@@ -72,9 +72,13 @@ template <typename R>
 bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned char>& blob) {
     std::memset(a, 0, sizeof(TileArgs<R>));
     if ((int)t.segs.size() < 1 || (int)t.segs.size() > TILE_MAXSEG) return false;
-    a->ntiles = 1ull << (nl - TILE_W);
+    a->ntiles = 1ull << (nl - TILE_W - __builtin_popcountll(t.fix_mask));
     a->gbase = t.gbase;
     a->synth = t.synth_index;
+    a->fixmask = t.fix_mask;
+    a->fixval = t.fix_val & t.fix_mask;
+    a->zmask = t.zero_mask;
+    a->zval = t.zero_val & t.zero_mask;
     a->bins = t.bins;
     a->nbq = t.nbins_q;
     a->fflags = (t.synth ? 1 : 0) | (t.nbins_q > 0 ? 2 : 0);
@@ -97,6 +101,8 @@ bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned 
         a->wpos[i] = t.wpos[i];
         wmask |= 1ull << t.wpos[i];
     }
+    if (t.zero_mask & ~wmask) return false;
+    if (t.fix_mask & (wmask | ~((nl >= 64 ? 0ull : 1ull << nl) - 1))) return false;  // fixed bits: local, outside W
     std::vector<TTerm<R>> terms;      // slot terms then L terms
     std::vector<TSlot> slots;
     std::vector<Cx<R>> mats, fac;

@@ -708,6 +708,56 @@ def test_simulate_matches_separate_calls(dt, name):
     check_close(x.cpu().numpy(), exp, dt)
 
 
+@pytest.mark.parametrize("dt", DTYPES, ids=["c128", "c64"])
+@pytest.mark.parametrize("n", [26, 28])
+def test_simulate_live_tiles_qft(dt, n):
+    """Three or more tile passes: after the synthesised first pass, the later
+    passes run only the tiles whose not-yet-windowed bits equal the basis bits
+    (the rest are zero in and zero out).  Closed form QFT|x> on sampled
+    amplitudes, marginals against the same closed form (uniform), and the
+    same run with every tile (QJ_LIVE_TILES-free separate calls) agrees."""
+    x = (0x2D5A3C9 * n + 12345) & ((1 << n) - 1)
+    tdt = TDT[dt]
+    t = torch.empty(2**n, dtype=tdt, device="cuda")
+    st = qjp.State(t, basis=None)
+    t.fill_(float("nan"))
+    qubits = [0, 5, n - 1]
+    p = st.simulate(x, C.qft(n).gates, qubits=qubits, fuse=True)
+    st.canonicalize()
+    st.sync()
+    rng = np.random.default_rng(n)
+    idx = np.unique(np.concatenate([rng.integers(0, 2**n, 20000), [0, 2**n - 1]])).astype(np.int64)
+    got = t[torch.from_numpy(idx).cuda()].cpu().numpy().astype(np.complex128)
+    m = (np.uint64(x) * idx.astype(np.uint64)) % np.uint64(2**n)
+    exp = 2 ** (-n / 2) * np.exp(2j * np.pi * m.astype(np.float64) / 2**n)
+    assert np.max(np.abs(got - exp)) < (1e-12 if dt == np.complex128 else 1e-5)
+    assert np.max(np.abs(p.cpu().numpy() - 1 / 8)) < (1e-12 if dt == np.complex128 else 1e-5)
+    assert not torch.isnan(t).any()
+
+
+@pytest.mark.parametrize("n", [26])
+def test_simulate_live_tiles_random(n):
+    """A random circuit over several tile passes: qj_simulate (live tiles)
+    equals reset + apply_circuit(fused, every tile) + probabilities."""
+    circ = C.random_circuit(n, 300, 11, max_targets=2, max_controls=1)
+    basis = 0x2F0F0F3 & ((1 << n) - 1)
+    qubits = [1, n - 2, n // 2]
+    ref = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    sr = qjp.State(ref, basis=basis)
+    sr.apply_circuit(circ.gates, fuse=True)
+    pr = sr.probabilities(qubits)
+    sr.canonicalize()
+    sr.sync()
+    x = torch.full((2**n,), float("nan"), dtype=torch.complex128, device="cuda")
+    st = qjp.State(x, basis=None)
+    p = st.simulate(basis, circ.gates, qubits=qubits, fuse=True)
+    st.canonicalize()
+    st.sync()
+    assert torch.max(torch.abs(x - ref)).item() <= 1e-12
+    assert np.max(np.abs(p.cpu().numpy() - pr.cpu().numpy())) <= 1e-12
+    del ref, x
+
+
 def test_simulate_fallbacks_and_no_readout():
     n = 15
     circ = C.qft(n)
