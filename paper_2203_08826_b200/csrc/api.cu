@@ -1532,7 +1532,10 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
                 Step& t = p->steps[i];
                 uint64_t wm = 0;
                 for (int j = 0; j < TILE_W; ++j) wm |= 1ull << t.tile.wpos[j];
-                if (i > 0) {
+                if (i == 0) {  // the synthesised pass: the one tile holding x is the grid
+                    t.tile.fix_mask = all & ~wm;
+                    t.tile.fix_val = basis & t.tile.fix_mask;
+                } else {
                     t.tile.fix_mask = all & ~windowed & ~wm;
                     t.tile.fix_val = basis & t.tile.fix_mask;
                     t.tile.zero_mask = wm & ~windowed;
