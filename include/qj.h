@@ -79,8 +79,14 @@ typedef struct qj_state_s* qj_state;
  * dtype `dt` on the current device) and, unless basis_index == QJ_KEEP, write
  * the basis state |basis_index> into it (|0..0> for 0).
  * `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
- * `nccl_comm` must be NULL in this build for a single-GPU state (see
- * qj_state_init_sharded for sharded states).
+ * `nccl_comm` = NULL for a single-GPU state; otherwise an ncclComm_t of P
+ * ranks (one process per GPU, P a power of two): the state is then rank
+ * r's shard of an n-qubit state sharded on its top log2(P) qubits, amps_dev
+ * holds 2^(n - log2 P) amplitudes, and gates on global qubits run through
+ * local<->global exchanges (grouped ncclSend/ncclRecv through a bounded
+ * staging ring; NCCL is dlopen'ed on first use).  Every rank must make the
+ * same sequence of calls.  (qj_state_init_sharded: P virtual shards in one
+ * process.)
  * Errors: INVALID_ARG (out or amps_dev NULL), CAPACITY (n < 1 or n > 40),
  * DTYPE, INDEX_OUT_OF_RANGE (basis_index >= 2^n), CUDA. */
 qj_status qj_state_init(qj_state* out, void* amps_dev, int n, qj_dtype dt,
@@ -252,7 +258,8 @@ typedef struct {
 
 /* Draw `nshots` outcomes from the distribution `probs_dev` (DEVICE, 2^nbits
  * fp64 weights, need not be normalised; negative / NaN entries count as 0;
- * sum < 16) with the counter-based generator Philox4x32-10 keyed by `seed`:
+ * the direct method needs their sum < 15.5 -- its CDF is 2^-60 fixed point --
+ * and returns INVALID_ARG otherwise, e.g. for raw histogram counts) with the counter-based generator Philox4x32-10 keyed by `seed`:
  * shot i of the direct method uses counter (i mod 2^32, i >> 32, 0, 0) (R27), chain c
  * step t of Metropolis uses counter (t, c, 1, 0) (R28), so results depend only
  * on (probs, nshots, seed, opts), never on the device or launch shape.

@@ -1351,9 +1351,12 @@ static qj_status sample_impl(const double* p, int nbits, uint64_t nshots, uint64
         uint64_t total = 0;
         if (e == cudaSuccess) e = cudaMemcpyAsync(&total, direct_total_ptr(buf, nb), sizeof(total), cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e == cudaSuccess && total != 0) e = run_direct_shots(buf, nb, nshots, seed, samples, counts, st, ls);
+        if (e == cudaSuccess && total != 0 && total != kTotalOverflow)
+            e = run_direct_shots(buf, nb, nshots, seed, samples, counts, st, ls);
         if (!scratch) cudaFreeAsync(buf, st);
         if (e != cudaSuccess) return cuda_fail(e, "direct sampler");
+        if (total == kTotalOverflow)
+            return fail(QJ_ERR_INVALID_ARG, "direct sampler: weights sum to >= 15.5 (normalise them; the 2^-60 fixed-point CDF holds totals below 16)");
         if (total == 0) return fail(QJ_ERR_ZERO_PROBABILITY, "all %llu probabilities are zero", (unsigned long long)nb);
         return QJ_OK;
     }
@@ -1450,13 +1453,19 @@ static qj_status run_sim(qj_state s, qj_state_s::CachedPlan& p) {
         });
         if (e != cudaSuccess) return cuda_fail(e, "simulate marginal");
     }
-    if (nb) {
-        e = by_dtype(s->dt, [&](auto z) {
-            using R = decltype(z);
-            return run_bins_to_out<R>(p.sim_bins, nb, p.out, s->stream, s->ls);
-        });
-        if (e != cudaSuccess) return cuda_fail(e, "simulate readout");
-    }
+    return QJ_OK;
+}
+// the bins -> caller's output conversion stays outside the cached graph, so
+// the output pointer is not part of the plan key (callers may pass a fresh
+// buffer every call)
+static qj_status run_sim_out(qj_state s, qj_state_s::CachedPlan& p, void* out) {
+    const size_t nb = p.nq > 0 ? (size_t)1 << p.nq : 0;
+    if (!nb) return QJ_OK;
+    cudaError_t e = by_dtype(s->dt, [&](auto z) {
+        using R = decltype(z);
+        return run_bins_to_out<R>(p.sim_bins, nb, out, s->stream, s->ls);
+    });
+    if (e != cudaSuccess) return cuda_fail(e, "simulate readout");
     return QJ_OK;
 }
 
@@ -1495,7 +1504,6 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
     key.push_back(basis);
     key.push_back((uint64_t)nq);
     for (int i = 0; i < nq; ++i) key.push_back((uint64_t)qubits[i]);
-    key.push_back((uint64_t)(uintptr_t)out_dev);
     qj_state_s::CachedPlan* p = nullptr;
     for (size_t i = 0; i < s->plans.size() && !p; ++i)
         if (s->plans[i]->key == key) {
@@ -1509,7 +1517,6 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
         p->sim = true;
         p->basis = basis;
         p->nq = nq;
-        p->out = out_dev;
         PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, 1, &s->phys};
         s->planner.plan(ctx, gs, true, p->steps);
         p->phys_after = s->phys;
@@ -1612,6 +1619,7 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
         const uint64_t before = s->ls.launches;
         if (qj_status q = run_sim(s, *p)) return q;
         p->kernels = s->ls.launches - before;
+        if (qj_status q = run_sim_out(s, *p, out_dev)) return q;
         p->uses = 1;
     } else {
         const uint64_t before = s->ls.launches;
@@ -1641,6 +1649,7 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
         } else if (qj_status q = run_sim(s, *p)) {
             return q;
         }
+        if (qj_status q = run_sim_out(s, *p, out_dev)) return q;
         p->uses++;
     }
     account(s, *p);

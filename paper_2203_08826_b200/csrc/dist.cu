@@ -98,8 +98,12 @@ cudaError_t launch_half_unpack(void* state, const void* buf, int amp_bytes, int 
 
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     const uint64_t n16 = bytes / 16;
-    copy16_kernel<<<grid_of(n16), 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
-    return cudaGetLastError();
+    if (n16) copy16_kernel<<<grid_of(n16), 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && bytes % 16)  // tail (e.g. one complex64 amplitude of a 2-amplitude shard)
+        e = cudaMemcpyAsync(static_cast<char*>(dst) + n16 * 16, static_cast<const char*>(src) + n16 * 16, bytes % 16,
+                            cudaMemcpyDeviceToDevice, st);
+    return e;
 }
 
 }  // namespace qj

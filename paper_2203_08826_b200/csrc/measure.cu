@@ -147,30 +147,56 @@ __device__ uint64_t tile_scan(const double* p, uint64_t nb, uint64_t tile, uint6
     return total;
 }
 
-__global__ void __launch_bounds__(kMT) scan_tiles_kernel(const double* p, uint64_t nb, uint64_t* tile_tot) {
+__global__ void __launch_bounds__(kMT) scan_tiles_kernel(const double* p, uint64_t nb, uint64_t* tile_tot,
+                                                         double* tile_dsum) {
     __shared__ uint64_t s[kScanTile + kScanTile / 16];
     __shared__ uint64_t wsum[kMT / 32];
-    const uint64_t t = tile_scan(p, nb, blockIdx.x, s, wsum);
-    if (threadIdx.x == 0) tile_tot[blockIdx.x] = t;
+    __shared__ double dsum[kMT / 32];
+    // fp64 weight of the tile, only to reject totals the 2^-60 fixed point cannot hold
+    double d = 0.0;
+    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+    for (int i = threadIdx.x; i < kScanTile; i += kMT)
+        if (base + i < nb && p[base + i] > 0.0) d += p[base + i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) dsum[threadIdx.x >> 5] = d;
+    const uint64_t t = tile_scan(p, nb, blockIdx.x, s, wsum);  // (its barriers order dsum)
+    if (threadIdx.x == 0) {
+        double e = 0.0;
+        for (int i = 0; i < kMT / 32; ++i) e += dsum[i];
+        tile_tot[blockIdx.x] = t;
+        tile_dsum[blockIdx.x] = e;
+    }
 }
 
 // exclusive scan of the tile totals in place (one block), total -> *total
-__global__ void __launch_bounds__(1024) scan_offsets_kernel(uint64_t* tot, uint64_t ntiles, uint64_t* total) {
+__global__ void __launch_bounds__(1024) scan_offsets_kernel(uint64_t* tot, const double* dsum, uint64_t ntiles,
+                                                            uint64_t* total) {
     __shared__ uint64_t part[1024];
+    __shared__ double dpart[1024];
     const uint64_t per = (ntiles + 1023) / 1024;
     const uint64_t b = threadIdx.x * per, e = min(ntiles, b + per);
     uint64_t run = 0;
-    for (uint64_t i = b; i < e; ++i) run += tot[i];
+    double drun = 0.0;
+    for (uint64_t i = b; i < e; ++i) {
+        run += tot[i];
+        drun += dsum[i];
+    }
     part[threadIdx.x] = run;
+    dpart[threadIdx.x] = drun;
     __syncthreads();
     if (threadIdx.x == 0) {
         uint64_t acc = 0;
+        double dacc = 0.0;
         for (int i = 0; i < 1024; ++i) {
             const uint64_t x = part[i];
             part[i] = acc;
             acc += x;
+            dacc += dpart[i];
         }
-        *total = acc;
+        // the fixed-point CDF holds totals below 2^64 = 16 * 2^60: larger
+        // weights would wrap; flag them for the host check (kTotalOverflow)
+        *total = (dacc >= 15.5 || !(dacc == dacc)) ? kTotalOverflow : acc;
     }
     __syncthreads();
     uint64_t acc = part[threadIdx.x];
@@ -294,7 +320,7 @@ cudaError_t run_collapse_apply(void* psi, int nl, uint64_t mask, uint64_t want, 
 
 size_t direct_scratch_bytes(uint64_t nb) {
     const uint64_t ntiles = (nb + kScanTile - 1) / kScanTile;
-    return (nb + ntiles + 1) * sizeof(uint64_t);
+    return (nb + ntiles + 1) * sizeof(uint64_t) + ntiles * sizeof(double);
 }
 
 cudaError_t run_direct_cdf(const double* p, uint64_t nb, void* scratch, cudaStream_t st, LaunchStats& ls) {
@@ -302,8 +328,9 @@ cudaError_t run_direct_cdf(const double* p, uint64_t nb, void* scratch, cudaStre
     uint64_t* cdf = static_cast<uint64_t*>(scratch);
     uint64_t* tot = cdf + nb;
     uint64_t* total = tot + ntiles;
-    scan_tiles_kernel<<<(unsigned)ntiles, kMT, 0, st>>>(p, nb, tot);
-    scan_offsets_kernel<<<1, 1024, 0, st>>>(tot, ntiles, total);
+    double* dsum = reinterpret_cast<double*>(total + 1);
+    scan_tiles_kernel<<<(unsigned)ntiles, kMT, 0, st>>>(p, nb, tot, dsum);
+    scan_offsets_kernel<<<1, 1024, 0, st>>>(tot, dsum, ntiles, total);
     scan_write_kernel<<<(unsigned)ntiles, kMT, 0, st>>>(p, nb, tot, cdf);
     ls.launches += 3;
     return cudaGetLastError();

@@ -37,6 +37,16 @@ struct Pass {
     std::vector<cd> m;             // DENSE: 4^k row-major; DIAG: 2^k; PHASE: 1
 };
 
+// Streaming multiprocessors of the current device (148 on B200); grids are
+// sized in multiples of it.
+inline int device_sms() {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        sms <= 0)
+        return 148;
+    return sms;
+}
+
 struct LaunchStats {
     uint64_t launches = 0;
 };
@@ -78,6 +88,7 @@ template <typename R>
 cudaError_t run_collapse_apply(void* psi, int nl, uint64_t mask, uint64_t want, double scale, cudaStream_t st,
                                LaunchStats& ls);
 size_t direct_scratch_bytes(uint64_t nbins);
+constexpr uint64_t kTotalOverflow = ~0ull;  // direct sampler: weights sum to >= 15.5 (the 2^-60 CDF would wrap)
 cudaError_t run_direct_cdf(const double* p, uint64_t nbins, void* scratch, cudaStream_t st, LaunchStats& ls);
 const uint64_t* direct_total_ptr(const void* scratch, uint64_t nbins);
 cudaError_t run_direct_shots(const void* scratch, uint64_t nbins, uint64_t nshots, uint64_t seed, int64_t* samples,

@@ -523,9 +523,7 @@ cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, Tile
         if (e != cudaSuccess) return e;
         attr = want;
     }
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     const uint64_t grid = std::min<uint64_t>(a->ntiles, (uint64_t)sms * TILE_MINBLOCKS);
     std::string jerr;
     const JitKernel* jk = tile_jit_kernel<R>(*a, blob.empty() ? nullptr : blob.data(), &jerr, nullptr);
@@ -566,9 +564,7 @@ cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out
         if (e != cudaSuccess) return e;
         attr = want;
     }
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     out.grid = (unsigned)std::min<uint64_t>(a->ntiles, (uint64_t)sms * TILE_MINBLOCKS);
     std::string jerr;
     const JitKernel* jk = tile_jit_kernel<R>(*a, blob.empty() ? nullptr : blob.data(), &jerr, nullptr);

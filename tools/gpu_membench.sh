@@ -1,4 +1,5 @@
 #!/bin/bash
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/membench tools/membench.cu || exit 1  # built on the box, never committed
 mkdir -p gpurun_out
 out=gpurun_out/membench.jsonl; : > $out
 for cfg in "3 21" "3 18" "3 12" "3 3" "4 22" "5 23" "6 24" "8 26" "12 12"; do
