@@ -199,7 +199,7 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
  * accumulated in a different order than qj_probabilities (agreement to fp64
  * rounding).  Otherwise it runs the three calls.  Plans (and, from the
  * second call on a non-default stream, a CUDA graph of the whole step) are
- * cached per (circuit, flags, basis, qubits, out_dev).  Errors: as the three
+ * cached per (circuit, flags, basis, qubits); out_dev is patched per call.  Errors: as the three
  * calls. */
 qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngates, uint32_t flags,
                       const int* qubits, int nq, void* out_dev);
@@ -213,6 +213,12 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
  * canonical order (R1) with SWAP passes / exchanges (two global bits trade
  * places by three exchanges through the top local bit) and resets the map. */
 qj_status qj_state_canonicalize(qj_state s);
+
+/* The current logical->physical map: phys[q] (n ints, caller-owned host
+ * memory) receives the bit of the global index (local bits first, then the
+ * global / shard bits) that holds qubit q; canonical = n-1-q.  Host-only
+ * read, no synchronisation.  Errors: INVALID_ARG (NULL). */
+qj_status qj_state_layout(qj_state s, int* phys);
 
 /* ---- readout -----------------------------------------------------------------
  * Born-rule probabilities.  qubits == NULL and nq == -1:
@@ -361,6 +367,15 @@ typedef struct {
 
 qj_status qj_plan_circuit(int n, int nshards, int amp_bytes, const qj_gate* gates, int ngates,
                           uint32_t flags, qj_plan_step* out, int max_steps, int* nsteps, int* phys);
+
+/* The steps qj_state_canonicalize runs on a state of n qubits in `nshards`
+ * shards whose logical->physical map is phys_in (n ints, a permutation):
+ * SWAP passes for local pairs (one per shard index), exchanges for
+ * local/global and global/global pairs; afterwards qubit q is at bit n-1-q.
+ * Host only.  Errors: INVALID_ARG (NULL, nshards not a power of two, phys_in
+ * not a permutation), CAPACITY (too many shards for n, > max_steps steps). */
+qj_status qj_plan_canonicalize(int n, int nshards, const int* phys_in, qj_plan_step* out, int max_steps,
+                               int* nsteps);
 
 /* The paper's gate fusion (Table 2 Gates* / Depth*), host
  * only: greedily combine the circuit into gates of at most `max_qubits` (1 or

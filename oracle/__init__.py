@@ -52,6 +52,9 @@ def lib():
         L.or_basis_state.restype = None
         L.or_probabilities.argtypes = [P, I, P, I, P]
         L.or_probabilities.restype = None
+        L.or_qft_basis_maxerr.argtypes = [P, I, I, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, P,
+                                          ctypes.POINTER(ctypes.c_double)]
+        L.or_qft_basis_maxerr.restype = ctypes.c_double
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = I
         _lib = L
@@ -108,3 +111,17 @@ def probabilities(psi: np.ndarray, n: int, qubits=None) -> np.ndarray:
     p = np.ascontiguousarray(psi, dtype=np.complex128)
     lib().or_probabilities(_ptr(p), n, _ptr(q), len(q), _ptr(out))
     return out
+
+
+def qft_basis_maxerr(psi: np.ndarray, n: int, x: int, offset: int = 0, phys=None):
+    """Closed-form QFT|x> check of a chunk of a state computed elsewhere
+    (or_qft_basis_maxerr): element j of `psi` (complex128 or complex64) is
+    buffer index offset + j; `phys` (qubit -> bit) gives a physical layout,
+    None = canonical order.  Returns (max abs error, sum of squared errors)."""
+    a = np.ascontiguousarray(psi)
+    assert a.dtype in (np.complex128, np.complex64)
+    ph = None if phys is None else _ints(phys)
+    ss = ctypes.c_double(0.0)
+    m = lib().or_qft_basis_maxerr(_ptr(a), int(a.dtype == np.complex64), n, int(x), int(offset), a.size,
+                                  _ptr(ph), ctypes.byref(ss))
+    return float(m), float(ss.value)

@@ -28,6 +28,7 @@
  * Parity pins for every function here: tests/test_oracle_pins.py.
  */
 #include <complex.h>
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -96,6 +97,61 @@ void or_probabilities(const cplx* psi, int n, const int* qubits, int nq, double*
         double re = creal(psi[i]), im = cimag(psi[i]);
         out[o] += re * re + im * im;
     }
+}
+
+/* Closed-form checker for the quantum Fourier transform of a basis state,
+ * the plain definition of what QFT|x> is (SURVEY 8(c) "QFT|x>" pin; the QFT
+ * circuit of SPEC S:502-510 with its final SWAP layer, R18):
+ *     amp(y) = 2^(-n/2) exp(2 pi i ((x y) mod 2^n) / 2^n).
+ * The phase numerator m = (x y) mod 2^n is an exact integer (uint64 product
+ * wraps modulo 2^64, and 2^n divides 2^64 for n <= 63); m / 2^n is exact in
+ * double and is reduced to [-1/2, 1/2) before the sine and cosine.
+ *
+ * Streams over a chunk of a state produced elsewhere: element j of `psi`
+ * (complex128, or complex64 when is_c64) is the amplitude at buffer index
+ * i = offset + j.  phys == NULL: i is the canonical basis index y.  Otherwise
+ * the buffer is in a physical layout: qubit q sits at bit phys[q] of i, so
+ * y = sum_q bit(i, phys[q]) << (n-1-q).  Returns max_j |psi_j - amp(y_j)|
+ * and adds sum_j |psi_j - amp(y_j)|^2 to *sumsq (may be NULL). */
+double or_qft_basis_maxerr(const void* psi, int is_c64, int n, uint64_t x, uint64_t offset, uint64_t len,
+                           const int* phys, double* sumsq)
+{
+    const double two_pi = 6.283185307179586476925286766559;
+    const double scale = ldexp(1.0, -n);
+    const double norm = sqrt(scale);  /* 2^(-n/2) */
+    const uint64_t mask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+    double worst = 0.0, ss = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : worst) reduction(+ : ss)
+    for (int64_t j = 0; j < (int64_t)len; ++j) {
+        const uint64_t i = offset + (uint64_t)j;
+        uint64_t y = i;
+        if (phys) {
+            y = 0;
+            for (int q = 0; q < n; ++q) y |= ((i >> phys[q]) & 1ull) << (n - 1 - q);
+        }
+        const uint64_t m = (x * y) & mask;
+        double f = (double)m * scale;          /* exact: m < 2^n, power-of-two scale */
+        if (f >= 0.5) f -= 1.0;                /* same angle, in [-1/2, 1/2) */
+        const double th = two_pi * f;
+        const double re = norm * cos(th), im = norm * sin(th);
+        double gr, gi;
+        if (is_c64) {
+            const float* a = (const float*)psi;
+            gr = a[2 * j];
+            gi = a[2 * j + 1];
+        } else {
+            const double* a = (const double*)psi;
+            gr = a[2 * j];
+            gi = a[2 * j + 1];
+        }
+        const double dr = gr - re, di = gi - im;
+        const double e2 = dr * dr + di * di;
+        const double e = sqrt(e2);
+        if (!(e <= worst)) worst = (e == e) ? e : INFINITY;  /* NaN counts as a failure */
+        ss += e2;
+    }
+    if (sumsq) *sumsq += ss;
+    return worst;
 }
 
 /* Number of OpenMP threads the oracle uses (reported as cpu_baseline.cores). */

@@ -1039,6 +1039,12 @@ qj_status qj_state_info(qj_state s, int* n, int* n_local, int* dtype, int* nshar
     return QJ_OK;
 }
 
+qj_status qj_state_layout(qj_state s, int* phys) {
+    if (!s || !phys) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
+    for (int q = 0; q < s->n; ++q) phys[q] = s->phys[q];
+    return QJ_OK;
+}
+
 qj_status qj_get_counters(qj_state s, qj_counters* out, int reset) {
     if (!s || !out) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
     s->ctr.launches = s->ls.launches;
@@ -1768,10 +1774,12 @@ qj_status qj_plan_circuit(int n, int nshards, int amp_bytes, const qj_gate* gate
     return QJ_OK;
 }
 
-qj_status qj_state_canonicalize(qj_state s) {
-    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
-    const int n = s->n, nl = s->nl;
-    std::vector<int> phys = s->phys;
+// Steps that bring the logical->physical map `phys` back to canonical
+// (qubit q at bit n-1-q) on `nshards` shards of 2^nl amplitudes: local pairs
+// by SWAP passes on EVERY shard index (each rank runs its own), local/global
+// pairs by one exchange, global pairs by three exchanges through the top
+// local bit.  `phys` is updated to the canonical map.
+static std::vector<Step> canonicalize_steps(int n, int nl, int nshards, int amp_bytes, std::vector<int>& phys) {
     std::vector<Step> steps;
     for (int q = 0; q < n; ++q) {
         const int want = n - 1 - q, cur = phys[q];
@@ -1779,15 +1787,15 @@ qj_status qj_state_canonicalize(qj_state s) {
         int q2 = 0;
         while (phys[q2] != want) ++q2;
         if (cur < nl && want < nl) {
-            for (size_t r = 0; r < s->shards.size(); ++r) {
+            for (int r = 0; r < nshards; ++r) {
                 Step st;
                 st.type = Step::PASS;
-                st.shard = (int)r;
+                st.shard = r;
                 st.pass.kind = PK_SWAP;
                 st.pass.k = 2;
                 st.pass.tpos[0] = cur;
                 st.pass.tpos[1] = want;
-                st.alg_bytes = pass_alg_bytes(st.pass, nl, s->amp_bytes);
+                st.alg_bytes = pass_alg_bytes(st.pass, nl, amp_bytes);
                 steps.push_back(std::move(st));
             }
         } else if (cur >= nl && want >= nl) {
@@ -1810,6 +1818,15 @@ qj_status qj_state_canonicalize(qj_state s) {
         phys[q] = want;
         phys[q2] = cur;
     }
+    return steps;
+}
+
+qj_status qj_state_canonicalize(qj_state s) {
+    if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
+    std::vector<int> phys = s->phys;
+    // total_shards(): an NCCL rank holds one shard but plans for all of them
+    // (execute() runs the steps of its own shard index only)
+    const std::vector<Step> steps = canonicalize_steps(s->n, s->nl, s->total_shards(), s->amp_bytes, phys);
     qj_status st = execute(s, steps);
     if (st == QJ_OK) s->phys = phys;
     if (st == QJ_OK && s->host) {  // put the half-slices back in the caller's buffer order
@@ -1818,6 +1835,41 @@ qj_status qj_state_canonicalize(qj_state s) {
         st = host_materialize(s);
     }
     return st;
+}
+
+qj_status qj_plan_canonicalize(int n, int nshards, const int* phys_in, qj_plan_step* out, int max_steps,
+                               int* nsteps) {
+    if (!phys_in || !nsteps || (max_steps > 0 && !out)) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
+    if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
+    if (nshards < 1 || (nshards & (nshards - 1))) return fail(QJ_ERR_INVALID_ARG, "nshards=%d is not a power of two", nshards);
+    int g = 0;
+    while ((1 << g) < nshards) ++g;
+    if (g >= n) return fail(QJ_ERR_CAPACITY, "%d shards need more than n=%d qubits", nshards, n);
+    std::vector<int> phys(phys_in, phys_in + n);
+    std::vector<int> seen(n, 0);
+    for (int q = 0; q < n; ++q) {
+        if (phys[q] < 0 || phys[q] >= n || seen[phys[q]]++) return fail(QJ_ERR_INVALID_ARG, "phys is not a permutation of 0..n-1");
+    }
+    const std::vector<Step> steps = canonicalize_steps(n, n - g, nshards, 16, phys);
+    if ((int)steps.size() > max_steps) return fail(QJ_ERR_CAPACITY, "plan has %zu steps > %d", steps.size(), max_steps);
+    for (size_t i = 0; i < steps.size(); ++i) {
+        const Step& st = steps[i];
+        qj_plan_step& o = out[i];
+        std::memset(&o, 0, sizeof(o));
+        o.type = (int)st.type;
+        o.shard = st.shard;
+        o.gbit = st.gbit;
+        o.lbit = st.lbit;
+        o.alg_bytes = st.alg_bytes;
+        if (st.type == Step::PASS) {
+            o.kind = st.pass.kind;
+            o.k = st.pass.k;
+            for (int j = 0; j < st.pass.k; ++j) o.tpos[j] = st.pass.tpos[j];
+            o.touch = st.pass.touch;
+        }
+    }
+    *nsteps = (int)steps.size();
+    return QJ_OK;
 }
 
 qj_status qj_sync(qj_state s) {

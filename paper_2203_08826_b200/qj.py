@@ -37,7 +37,7 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
            "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit", "qj_collapse",
            "qj_sample_distribution", "qj_sample", "qj_measure", "qj_state_init_host",
-           "qj_simulate"]
+           "qj_simulate", "qj_state_layout", "qj_plan_canonicalize"]
 
 
 class QJError(RuntimeError):
@@ -111,6 +111,7 @@ def lib():
         "qj_sync": ([P], S),
         "qj_get_counters": ([P, ctypes.POINTER(qj_counters), I], S),
         "qj_state_info": ([P, IP, IP, IP, IP], S),
+        "qj_state_layout": ([P, IP], S),
         "qj_last_error": ([], ctypes.c_char_p),
         "qj_version": ([], ctypes.c_char_p),
         "qj_insert_zero_bits": ([U64, IP, I], U64),
@@ -120,6 +121,7 @@ def lib():
         "qj_plan_circuit": ([I, I, I, ctypes.POINTER(qj_gate), I, ctypes.c_uint32, ctypes.POINTER(qj_plan_step), I,
                              IP, IP], S),
         "qj_exchange_peer": ([I, I, IP, IP], None),
+        "qj_plan_canonicalize": ([I, I, IP, ctypes.POINTER(qj_plan_step), I, IP], S),
         "qj_fuse_circuit": ([I, ctypes.POINTER(qj_gate), I, I, ctypes.POINTER(qj_gate), ctypes.POINTER(ctypes.c_double),
                              I, IP, IP], S),
         "qj_collapse": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_double)], S),
@@ -264,6 +266,17 @@ def plan_circuit(n, nshards, gates, fuse=False, amp_bytes=16, max_steps=1 << 16)
                       "fix": [(o.fpos[j], o.fval[j]) for j in range(o.nfix)], "touch": o.touch, "m": m,
                       "gbit": o.gbit, "lbit": o.lbit, "alg_bytes": o.alg_bytes})
     return steps, list(phys)
+
+
+def plan_canonicalize(n, nshards, phys, max_steps=4096):
+    """The steps qj_state_canonicalize runs for map `phys` (host only)."""
+    out = (qj_plan_step * max_steps)()
+    cnt = ctypes.c_int()
+    ph = (ctypes.c_int * n)(*phys)
+    _check(lib().qj_plan_canonicalize(n, nshards, ph, out, max_steps, ctypes.byref(cnt)))
+    return [{"type": out[i].type, "shard": out[i].shard, "kind": out[i].kind, "tpos": list(out[i].tpos[:out[i].k]),
+             "fix": [], "touch": out[i].touch, "m": np.zeros(0, np.complex128), "gbit": out[i].gbit,
+             "lbit": out[i].lbit, "alg_bytes": out[i].alg_bytes} for i in range(cnt.value)]
 
 
 class FusedGate:
@@ -561,6 +574,12 @@ class State:
         _check(lib().qj_get_profile(self._h, arr, 16, ctypes.byref(cnt), 1 if reset else 0))
         return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
                                        "alg_bytes": arr[i].alg_bytes} for i in range(cnt.value)}
+
+    def layout(self):
+        """Logical->physical bit map: qubit q is held at bit layout()[q]."""
+        phys = (ctypes.c_int * self.n)()
+        _check(lib().qj_state_layout(self._h, phys))
+        return list(phys)
 
     def info(self):
         v = [ctypes.c_int() for _ in range(4)]

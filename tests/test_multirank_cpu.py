@@ -83,7 +83,30 @@ def apply_pass(psi, nl, st):
     return out
 
 
-def _worker(rank, world, port, n, seed, which, result_q):
+def _run_steps(steps, shard, rank, nl, Q):
+    nex = 0
+    for st in steps:
+        if st["type"] == 0:
+            if st["shard"] == rank:
+                shard = apply_pass(shard, nl, st)
+        elif st["type"] == 1:
+            nex += 1
+            peer, hb = Q.exchange_peer(rank, st["gbit"])
+            L = st["lbit"]
+            idx = np.arange(shard.size)
+            sel = np.nonzero(((idx >> L) & 1) == hb)[0]
+            send = torch.from_numpy(np.ascontiguousarray(shard[sel]).view(np.float64))
+            recv = torch.empty_like(send)
+            req = dist.isend(send, peer)
+            dist.recv(recv, peer)
+            req.wait()
+            shard[sel] = recv.numpy().view(np.complex128)
+        else:
+            raise AssertionError("unexpected fused step")
+    return shard, nex
+
+
+def _worker(rank, world, port, n, seed, which, result_q, canon=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -100,25 +123,10 @@ def _worker(rank, world, port, n, seed, which, result_q):
         full /= np.linalg.norm(full)
         shard = full[rank << nl:(rank + 1) << nl].copy()
         steps, phys = Q.plan_circuit(n, world, circ.gates)
-        nex = 0
-        for st in steps:
-            if st["type"] == 0:
-                if st["shard"] == rank:
-                    shard = apply_pass(shard, nl, st)
-            elif st["type"] == 1:
-                nex += 1
-                peer, hb = Q.exchange_peer(rank, st["gbit"])
-                L = st["lbit"]
-                idx = np.arange(shard.size)
-                sel = np.nonzero(((idx >> L) & 1) == hb)[0]
-                send = torch.from_numpy(np.ascontiguousarray(shard[sel]).view(np.float64))
-                recv = torch.empty_like(send)
-                req = dist.isend(send, peer)
-                dist.recv(recv, peer)
-                req.wait()
-                shard[sel] = recv.numpy().view(np.complex128)
-            else:
-                raise AssertionError("unexpected fused step")
+        shard, nex = _run_steps(steps, shard, rank, nl, Q)
+        if canon:  # qj_state_canonicalize's plan: every rank ends in canonical order
+            shard, _ = _run_steps(Q.plan_canonicalize(n, world, phys), shard, rank, nl, Q)
+            phys = [n - 1 - q for q in range(n)]
         parts = [torch.empty(2 * shard.size, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(shard.view(np.float64)))
         if rank == 0:
@@ -136,11 +144,11 @@ def _worker(rank, world, port, n, seed, which, result_q):
         dist.destroy_process_group()
 
 
-def _run(world, n, seed, which):
+def _run(world, n, seed, which, canon=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, seed, which, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, seed, which, q, canon)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -172,3 +180,37 @@ def test_exchange_rule_pairs_up():
                 assert back == r and peer != r
                 assert hb + hb2 == 1  # the two halves traded are complementary
                 assert hb == 1 - ((r >> j) & 1)
+
+
+@pytest.mark.parametrize("world,seed", [(2, 11), (4, 12)])
+def test_canonicalize_plan_per_rank(world, seed):
+    """After a circuit that remaps global qubits, every rank runs
+    qj_state_canonicalize's plan for its own shard index (SWAP passes on
+    local pairs are emitted for every shard, not only shard 0); the gathered
+    shards are then the oracle's state in canonical order."""
+    err, nex = _run(world, 8, seed, "random", canon=True)
+    assert err < 1e-12, err
+    assert nex > 0
+
+
+def test_canonicalize_plan_covers_every_shard():
+    from paper_2203_08826_b200 import qj as Q
+    n, world = 9, 4
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        phys = [int(b) for b in rng.permutation(n)]
+        steps = Q.plan_canonicalize(n, world, phys)
+        passes = [s for s in steps if s["type"] == 0]
+        for i in range(0, len(passes), world):
+            assert sorted(s["shard"] for s in passes[i:i + world]) == list(range(world))
+        # replaying the plan on the map gives the canonical map
+        cur = list(phys)
+        for s in steps:
+            if s["type"] == 0:
+                if s["shard"] == 0:
+                    a, b = s["tpos"]
+                    cur = [b if p == a else a if p == b else p for p in cur]
+            else:  # exchange: global bit nl + gbit <-> local bit lbit (nl = n - 2 at 4 shards)
+                gb, b = (n - 2) + s["gbit"], s["lbit"]
+                cur = [b if p == gb else gb if p == b else p for p in cur]
+        assert cur == [n - 1 - q for q in range(n)], (phys, cur)

@@ -273,3 +273,61 @@ def test_bv_marginal(n):
     psi = run(C.bv(n))
     p = oracle.probabilities(psi, n, list(range(n - 1)))
     assert abs(p[-1] - 1) < 1e-10
+
+
+# ---------------------------------------------------------------- QFT|x> closed-form checker
+# oracle.qft_basis_maxerr (or_qft_basis_maxerr) streams the full-size GPU
+# states through the closed form; pinned here to a textbook library routine
+# (numpy's inverse FFT: QFT|x> = sqrt(N) ifft(e_x)), to the gate-by-gate
+# oracle, and to mutations it must reject.
+@pytest.mark.parametrize("n,x", [(1, 1), (4, 11), (7, 0b1011001), (10, 0b1011001110), (12, 2**12 - 1)])
+def test_qft_checker_vs_numpy_ifft(n, x):
+    e = np.zeros(2**n, dtype=np.complex128)
+    e[x] = 1.0
+    ref = np.sqrt(2**n) * np.fft.ifft(e)
+    m, ss = oracle.qft_basis_maxerr(ref, n, x)
+    assert m < 1e-15 and ss < 1e-28
+    got = run(C.qft(n), x) if n <= 10 else None
+    if got is not None:
+        assert oracle.qft_basis_maxerr(got, n, x)[0] < 1e-14
+
+
+def test_qft_checker_rejects_mutations():
+    n, x = 9, 0b100110101
+    e = np.zeros(2**n, dtype=np.complex128)
+    e[x] = 1.0
+    ref = np.sqrt(2**n) * np.fft.ifft(e)
+    bad = ref.copy()
+    bad[300] += 1e-9
+    assert oracle.qft_basis_maxerr(bad, n, x)[0] >= 0.99e-9
+    assert oracle.qft_basis_maxerr(np.conj(ref), n, x)[0] > 1e-3        # wrong sign of the phase
+    rev = np.array([ref[int(format(i, f"0{n}b")[::-1], 2)] for i in range(2**n)])
+    assert oracle.qft_basis_maxerr(rev, n, x)[0] > 1e-3                 # missing final SWAP layer
+    assert oracle.qft_basis_maxerr(ref, n, x ^ 1)[0] > 1e-3             # other basis input
+    nan = ref.copy()
+    nan[5] = np.nan
+    assert not oracle.qft_basis_maxerr(nan, n, x)[0] < 1.0              # NaN is a failure
+    # chunks: offsets address the same amplitudes
+    assert oracle.qft_basis_maxerr(ref[100:200], n, x, offset=100)[0] < 1e-15
+    assert oracle.qft_basis_maxerr(ref[100:200], n, x, offset=101)[0] > 1e-3
+    # complex64 buffers are widened, not reinterpreted
+    m64 = oracle.qft_basis_maxerr(ref.astype(np.complex64), n, x)[0]
+    assert 1e-10 < m64 < 1e-7
+
+
+def test_qft_checker_physical_layout():
+    n, x = 8, 0b11010011
+    rng = np.random.default_rng(5)
+    e = np.zeros(2**n, dtype=np.complex128)
+    e[x] = 1.0
+    ref = np.sqrt(2**n) * np.fft.ifft(e)
+    phys = [int(b) for b in rng.permutation(n)]  # qubit q at bit phys[q]
+    buf = np.empty_like(ref)
+    for y in range(2**n):
+        i = sum(((y >> (n - 1 - q)) & 1) << phys[q] for q in range(n))
+        buf[i] = ref[y]
+    assert oracle.qft_basis_maxerr(buf, n, x, phys=phys)[0] < 1e-15
+    assert oracle.qft_basis_maxerr(buf, n, x)[0] > 1e-3
+    wrong = list(phys)
+    wrong[0], wrong[1] = wrong[1], wrong[0]
+    assert oracle.qft_basis_maxerr(buf, n, x, phys=wrong)[0] > 1e-3

@@ -206,8 +206,6 @@ def random_gate(n: int, rng: np.random.Generator, max_targets: int = 3,
     targets = tuple(qs[:k])
     nc = int(rng.integers(0, min(max_controls, n - k) + 1))
     controls = tuple(qs[k:k + nc])
-    if kind == "fsim" and nc:
-        controls = ()  # fSim entry point takes controls too, but keep it plain here
     if kind == "dense":
         return G.unitary("U", targets, G.random_unitary(k, rng), controls)
     if kind == "x":
@@ -218,7 +216,7 @@ def random_gate(n: int, rng: np.random.Generator, max_targets: int = 3,
         return G.SWAP(targets[0], targets[1], controls)
     if kind == "fsim":
         th, ph = rng.uniform(0, 2 * math.pi, 2)
-        return G.FSIM(targets[0], targets[1], float(th), float(ph))
+        return G.FSIM(targets[0], targets[1], float(th), float(ph), controls)
     d = np.exp(1j * rng.uniform(0, 2 * math.pi, 2**k))
     if rng.random() < 0.3:
         d[:-1] = 1.0  # single non-unit entry: the CU1/CZ-like phase shape

@@ -175,11 +175,12 @@ def SWAP(a, b, controls=()):
     return Gate("SWAP" if not controls else "CSWAP", "swap", (a, b), tuple(controls))
 
 
-def FSIM(a, b, theta, phi):
-    """fSim(theta, phi) = [[1,0,0,0],[0,c,-is,0],[0,-is,c,0],[0,0,0,e^{-i phi}]]."""
+def FSIM(a, b, theta, phi, controls=()):
+    """fSim(theta, phi) = [[1,0,0,0],[0,c,-is,0],[0,-is,c,0],[0,0,0,e^{-i phi}]]
+    (optionally controlled: acts where every control qubit is 1)."""
     c, s = math.cos(theta), math.sin(theta)
     u = np.array([[c, -1j * s], [-1j * s, c]], dtype=np.complex128)
-    return Gate("FSIM", "fsim", (a, b), (), (u, complex(np.exp(-1j * phi))))
+    return Gate("FSIM", "fsim", (a, b), tuple(controls), (u, complex(np.exp(-1j * phi))))
 
 
 def RZZ(a, b, gamma):
