@@ -226,7 +226,12 @@ qj_status qj_state_layout(qj_state s, int* phys);
  * the marginal over the listed qubits, first listed = most significant bit of
  * the output index (2^nq values, accumulated in fp64).  `out_dev` is caller
  * owned DEVICE memory of the state's real type (float for C64, double for
- * C128).  Sharded states: out_dev must hold the full output. */
+ * C128).  Virtual-rank sharded states: out_dev must hold the full output.
+ * NCCL-sharded states: the full vector is distributed -- rank r's out_dev
+ * receives the canonical slice [r 2^n_local, (r+1) 2^n_local); if global
+ * qubits were remapped the state is first canonicalised in place
+ * (qj_state_canonicalize: exchanges, collective over the ranks); marginals
+ * are all-reduced and replicated on every rank. */
 qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev);
 
 /* ---- measurement ("a custom operator for collapsing and

@@ -55,6 +55,8 @@ def lib():
         L.or_qft_basis_maxerr.argtypes = [P, I, I, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, P,
                                           ctypes.POINTER(ctypes.c_double)]
         L.or_qft_basis_maxerr.restype = ctypes.c_double
+        L.or_set_num_threads.argtypes = [I]
+        L.or_set_num_threads.restype = None
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = I
         _lib = L
@@ -71,6 +73,10 @@ def _ints(xs):
 
 def num_threads() -> int:
     return int(lib().or_num_threads())
+
+
+def set_num_threads(t: int) -> None:
+    lib().or_set_num_threads(int(t))
 
 
 def basis_state(n: int, x: int = 0) -> np.ndarray:

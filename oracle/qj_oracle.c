@@ -154,6 +154,17 @@ double or_qft_basis_maxerr(const void* psi, int is_c64, int n, uint64_t x, uint6
     return worst;
 }
 
+/* Set the OpenMP thread count for later calls (bench.py times the oracle on
+ * all host cores and on one). */
+void or_set_num_threads(int t)
+{
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}
+
 /* Number of OpenMP threads the oracle uses (reported as cpu_baseline.cores). */
 int or_num_threads(void)
 {

@@ -62,6 +62,10 @@ struct qj_state_s {
     int rank = 0, nranks = 1;
     void* xbuf = nullptr;  // exchange staging ring
     size_t xbuf_bytes = 0;
+    // exchange pipeline: NCCL transfers on their own stream, so chunk c's
+    // transfer overlaps chunk c+1's pack and chunk c-1's unpack
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t xev_in[2] = {}, xev_out[2] = {}, xev_start = nullptr;
     void* mbuf = nullptr;  // measurement scratch (norm partials, sampler CDF); never in a captured graph
     size_t mbuf_bytes = 0;
     // host-staged states (row f4): `shards` are HOST slices;
@@ -302,32 +306,59 @@ qj_status nccl_exchange(qj_state s, int j, int L) {
         if (e != cudaSuccess) return cuda_fail(e, "exchange staging alloc");
         s->xbuf_bytes = need;
     }
+    if (!s->xstream) {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->xstream, cudaStreamNonBlocking);
+        for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+            e = cudaEventCreateWithFlags(&s->xev_in[k], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->xev_out[k], cudaEventDisableTiming);
+        }
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->xev_start, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "exchange stream");
+    }
     unsigned char* state = static_cast<unsigned char*>(s->shards[0]);
     unsigned char* stage = static_cast<unsigned char*>(s->xbuf);
     ncclComm_t comm = static_cast<ncclComm_t>(s->comm);
     const uint64_t base = (uint64_t)ex.half_bit << (s->nl - 1);  // contiguous case
-    cudaError_t e;
+    // Pipeline over chunks, two staging slots:
+    //   compute stream: [pack c -> slot c&1] ... [unpack slot c&1 -> state]
+    //   exchange stream:        [send c / recv c into slot c&1]
+    // xev_in[k]:  slot k's send data is ready (pack done, or the state itself
+    //             is ready) and its receive buffer is free (unpack c-2 done);
+    // xev_out[k]: chunk c's transfer finished (the unpack may read slot k and
+    //             overwrite the amplitudes it sent).
+    // The compute stream waits for the last transfer before its last unpack,
+    // so both streams join there (also inside a captured CUDA graph).
+    cudaError_t e = cudaEventRecord(s->xev_start, s->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s->xstream, s->xev_start, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "exchange fork");
     for (uint64_t h0 = 0, c = 0; h0 < half; h0 += chunk, ++c) {
+        const int k = (int)(c & 1);
         const uint64_t cnt = std::min<uint64_t>(chunk, half - h0);
         const size_t bytes = (size_t)cnt * s->amp_bytes;
-        unsigned char* recv = stage + (c & 1) * cb;
+        unsigned char* recv = stage + k * cb;
         const unsigned char* send;
         if (contiguous) {
             send = state + (size_t)(base + h0) * s->amp_bytes;
         } else {
-            unsigned char* pk = stage + (2 + (c & 1)) * cb;
+            unsigned char* pk = stage + (2 + k) * cb;
             e = launch_half_pack(state, pk, s->amp_bytes, L, ex.half_bit, h0, cnt, s->stream);
             if (e != cudaSuccess) return cuda_fail(e, "exchange pack");
             s->ls.launches++;
             send = pk;
         }
+        e = cudaEventRecord(s->xev_in[k], s->stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s->xstream, s->xev_in[k], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "exchange order");
         ncclResult_t r = api->GroupStart();
-        if (r == ncclSuccess) r = api->Send(send, bytes, ncclInt8, ex.peer, comm, s->stream);
-        if (r == ncclSuccess) r = api->Recv(recv, bytes, ncclInt8, ex.peer, comm, s->stream);
+        if (r == ncclSuccess) r = api->Send(send, bytes, ncclInt8, ex.peer, comm, s->xstream);
+        if (r == ncclSuccess) r = api->Recv(recv, bytes, ncclInt8, ex.peer, comm, s->xstream);
         const ncclResult_t r2 = api->GroupEnd();
         if (r != ncclSuccess || r2 != ncclSuccess)
             return fail(QJ_ERR_NCCL, "exchange send/recv with rank %d: %s", ex.peer,
                         api->GetErrorString(r != ncclSuccess ? r : r2));
+        e = cudaEventRecord(s->xev_out[k], s->xstream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s->stream, s->xev_out[k], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "exchange order");
         if (contiguous) e = launch_copy(state + (size_t)(base + h0) * s->amp_bytes, recv, bytes, s->stream);
         else e = launch_half_unpack(state, recv, s->amp_bytes, L, ex.half_bit, h0, cnt, s->stream);
         if (e != cudaSuccess) return cuda_fail(e, "exchange unpack");
@@ -1011,6 +1042,15 @@ qj_status qj_state_free(qj_state s) {
     if (s->scratch) cudaFree(s->scratch);
     if (s->bins) cudaFree(s->bins);
     if (s->xbuf) cudaFree(s->xbuf);
+    if (s->xstream) {
+        cudaStreamSynchronize(s->xstream);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(s->xev_in[k]);
+            cudaEventDestroy(s->xev_out[k]);
+        }
+        cudaEventDestroy(s->xev_start);
+        cudaStreamDestroy(s->xstream);
+    }
     if (s->mbuf) cudaFree(s->mbuf);
     if (s->hp.ready) {
         cudaStreamSynchronize(s->hp.h2d);
@@ -1190,8 +1230,13 @@ qj_status qj_probabilities(qj_state s, const int* qubits, int nq, void* out_dev)
         bool identity = true;
         for (int q = 0; q < n; ++q) identity &= (s->phys[q] == n - 1 - q);
         const size_t rb = s->dt == QJ_C64 ? 4 : 8;
-        if (s->comm && !identity)
-            return fail(QJ_ERR_UNSUPPORTED, "full probabilities of a remapped NCCL-sharded state: call qj_state_canonicalize first");
+        if (s->comm && !identity) {
+            // rank r's output is the canonical slice [r 2^nl, (r+1) 2^nl), which a
+            // remapped layout spreads over every rank: move the data back to the
+            // canonical layout first (exact moves; the logical state is unchanged)
+            if (qj_status st = qj_state_canonicalize(s)) return st;
+            identity = true;
+        }
         auto one = [&](size_t i, const void* src) -> cudaError_t {
             const uint64_t r = s->comm ? (uint64_t)s->rank : (uint64_t)i;
             if (identity) {

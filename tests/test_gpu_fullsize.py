@@ -80,7 +80,8 @@ def test_qft30_simulate_every_amplitude(dt):
     packed = st.pack_circuit(C.qft(n).gates)
     q = list(range(10))
     for _ in range(3):
-        t.fill_(float("nan"))  # nothing stale can pass
+        with torch.cuda.stream(stream):
+            t.fill_(float("nan"))  # nothing stale can pass (ordered on the state's stream)
         p = st.simulate(SEED_X, qubits=q, packed=packed)
         st.sync()
     phys = st.layout()
