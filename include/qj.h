@@ -324,7 +324,9 @@ qj_status qj_get_counters(qj_state s, qj_counters* out, int reset);
  * ("gate_dense", "gate_x", "gate_swap", "diag_table", "diag_phase",
  * "diag_neg", "tile", "exchange"), the number of launches, their summed
  * device time and their summed algorithmic bytes.  `count` receives the
- * number of entries written (<= max_entries). */
+ * number of entries written (<= max_entries).  `reset` bit 0: clear the
+ * records afterwards; bit 1: return one entry per recorded launch instead,
+ * in enqueue order (launches = 1). */
 typedef struct {
     char name[32];
     uint64_t launches;

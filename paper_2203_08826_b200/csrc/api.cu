@@ -1008,7 +1008,20 @@ qj_status qj_get_profile(qj_state s, qj_profile_entry* out, int max_entries, int
         bytes[r.kind] += r.bytes;
     }
     int c = 0;
-    for (int k = 0; k < PROF_N && c < max_entries; ++k) {
+    if (reset & 2) {  // one entry per recorded launch, in enqueue order
+        for (auto& r : s->recs) {
+            if (c >= max_entries) break;
+            float t = 0.f;
+            cudaEventElapsedTime(&t, r.a, r.b);
+            std::memset(&out[c], 0, sizeof(out[c]));
+            std::strncpy(out[c].name, kProfNames[r.kind], sizeof(out[c].name) - 1);
+            out[c].launches = 1;
+            out[c].total_ms = t;
+            out[c].alg_bytes = r.bytes;
+            ++c;
+        }
+    }
+    for (int k = 0; k < PROF_N && c < max_entries && !(reset & 2); ++k) {
         if (!launches[k]) continue;
         std::memset(&out[c], 0, sizeof(out[c]));
         std::strncpy(out[c].name, kProfNames[k], sizeof(out[c].name) - 1);
@@ -1018,7 +1031,7 @@ qj_status qj_get_profile(qj_state s, qj_profile_entry* out, int max_entries, int
         ++c;
     }
     *count = c;
-    if (reset) {
+    if (reset & 1) {
         for (auto& r : s->recs) {
             s->pool.push_back(r.a);
             s->pool.push_back(r.b);

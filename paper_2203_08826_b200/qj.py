@@ -581,6 +581,13 @@ class State:
         _check(lib().qj_state_layout(self._h, phys))
         return list(phys)
 
+    def profile_launches(self, reset=True):
+        """Per-launch records in enqueue order: [(kind, ms, alg_bytes)]."""
+        arr = (qj_profile_entry * 4096)()
+        cnt = ctypes.c_int()
+        _check(lib().qj_get_profile(self._h, arr, 4096, ctypes.byref(cnt), (1 if reset else 0) | 2))
+        return [(arr[i].name.decode(), arr[i].total_ms, arr[i].alg_bytes) for i in range(cnt.value)]
+
     def info(self):
         v = [ctypes.c_int() for _ in range(4)]
         _check(lib().qj_state_info(self._h, *[ctypes.byref(x) for x in v]))

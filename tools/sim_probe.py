@@ -10,14 +10,15 @@ import torch  # noqa: E402
 import paper_2203_08826_b200 as qj  # noqa: E402
 from workloads import circuits as C  # noqa: E402
 
-n = 30
-x = 0b101101110001011100101101011011
-circ = C.qft(n)
-t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+import bench  # noqa: E402
+
+wl = bench.make_workload(sys.argv[1] if len(sys.argv) > 1 else "qft30_c128")
+n, x, circ = wl["n"], wl["basis"], wl["circ"]
+t = torch.empty(2**n, dtype=torch.complex128 if wl["dtype"] == "c128" else torch.complex64, device="cuda")
 stream = torch.cuda.Stream()
 st = qj.State(t, basis=0, stream=stream)
 packed = st.pack_circuit(circ.gates)
-pb = torch.empty(1024, dtype=torch.float64, device="cuda")
+pb = torch.empty(1024, dtype=st.real_dtype, device="cuda")
 q = list(range(10))
 
 
@@ -48,6 +49,7 @@ st.set_profiling(True)
 for name, f in (("separate", sep), ("simulate", sim)):
     st.profile(reset=True)
     f()
-    res[name + "_passes"] = st.profile_events() if hasattr(st, "profile_events") else st.profile(reset=True)
+    res[name + "_launches"] = [(k, round(ms, 4), round(b / ms / 1e6 / 6450.9, 3) if ms > 0 else None)
+                               for k, ms, b in st.profile_launches(reset=True)]
 st.set_profiling(False)
 print(json.dumps(res))
