@@ -178,6 +178,11 @@ typedef struct {
 #define QJ_FUSE 1u       /* plan runs of gates into fused window tile passes */
 #define QJ_FUSE_GATES 2u /* first apply the paper's greedy fusion into <= 2-qubit
                             dense gates; combinable with QJ_FUSE */
+/* QJ_FUSE_GATES with a fusion width k in 1..5 (bits 4-7; 0 = 2, the paper's):
+ * "fusing gates up to about five [qubits] may provide additional advantage"
+ * (PAPER.md:574-575).  complex64 dense fused gates of 4-5 qubits run as
+ * tensor-core contractions (3xTF32 tcgen05.mma). */
+#define QJ_FUSE_GATES_K(k) (QJ_FUSE_GATES | (((uint32_t)(k) & 15u) << 4))
 
 /* Apply `ngates` gates in order.  Without QJ_FUSE every gate is one pass as
  * if issued through the single-gate entry points.  With QJ_FUSE the planner
@@ -385,10 +390,11 @@ qj_status qj_plan_canonicalize(int n, int nshards, const int* phys_in, qj_plan_s
                                int* nsteps);
 
 /* The paper's gate fusion (Table 2 Gates* / Depth*), host
- * only: greedily combine the circuit into gates of at most `max_qubits` (1 or
- * 2) qubits.  Fused groups come back as QJ_GATE_DENSE gates whose matrices
- * (complex128, row-major, first target = MSB) are written to `mats` (caller
- * buffer of 32 doubles per output gate) and pointed to by `data`; gates on more
+ * only: greedily combine the circuit into gates of at most `max_qubits` (1 to
+ * 5; the paper's fusion is 2) qubits.  Fused groups come back as
+ * QJ_GATE_DENSE gates whose matrices (complex128, row-major, first target =
+ * MSB) are written to `mats` (caller buffer of 2 * 4^max_qubits doubles per
+ * output gate: 32 for the paper's 2) and pointed to by `data`; gates on more
  * qubits are copied unchanged (their `data` still points at the caller's
  * input).  Gate data are read as complex128.  Errors: as qj_apply_circuit,
  * CAPACITY if more than max_out gates. */

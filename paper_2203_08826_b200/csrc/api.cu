@@ -41,6 +41,12 @@ static qj_status cuda_fail(cudaError_t e, const char* where) {
     return fail(QJ_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
+// QJ_FUSE_GATES_K(k): fusion width in flag bits 4-7 (0 = the paper's 2)
+static int fuse_width(uint32_t flags) {
+    const int k = (int)((flags >> 4) & 15u);
+    return k ? k : 2;
+}
+
 // ------------------------------------------------------------------ handle
 struct qj_state_s {
     int n = 0, nl = 0, g = 0;
@@ -790,6 +796,7 @@ qj_status apply_circuit_cached(qj_state s, const qj_gate* gates, int ngates, uin
     auto* p = new qj_state_s::CachedPlan;
     p->key.swap(key);
     PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, s->total_shards(), &s->phys};
+    s->planner.auto_fuse_ = !(flags & QJ_FUSE_GATES);
     s->planner.plan(ctx, gs, (flags & QJ_FUSE) != 0, p->steps);
     for (const Step& st : p->steps) {
         if (st.type == Step::TILE) {
@@ -1158,7 +1165,8 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
     if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
     if (ngates < 0) return fail(QJ_ERR_INVALID_ARG, "ngates=%d < 0", ngates);
     if (ngates > 0 && !gates) return fail(QJ_ERR_INVALID_ARG, "gates is NULL");
-    if (flags & ~(QJ_FUSE | QJ_FUSE_GATES)) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    if (flags & ~(QJ_FUSE | QJ_FUSE_GATES | 0xF0u)) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    if (fuse_width(flags) > 5) return fail(QJ_ERR_INVALID_ARG, "fusion width %d > 5", fuse_width(flags));
     std::vector<LGate> gs((size_t)ngates);
     for (int i = 0; i < ngates; ++i) {
         const qj_gate& g = gates[i];
@@ -1170,10 +1178,11 @@ qj_status qj_apply_circuit(qj_state s, const qj_gate* gates, int ngates, uint32_
             return st;
         }
     }
-    if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, s->n, 2);
+    if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, s->n, fuse_width(flags));
     bool done = false;
     if (qj_status st = apply_circuit_cached(s, gates, ngates, flags, gs, &done)) return st;
     if (done) return QJ_OK;
+    s->planner.auto_fuse_ = !(flags & QJ_FUSE_GATES);
     return apply_lgates(s, gs, (flags & QJ_FUSE) != 0);
 }
 
@@ -1539,7 +1548,8 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
     if (s->n < 64 && basis >= (1ull << s->n))
         return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "basis_index %llu >= 2^%d", (unsigned long long)basis, s->n);
     if (ngates < 0 || (ngates > 0 && !gates)) return fail(QJ_ERR_INVALID_ARG, "bad gate list");
-    if (flags & ~(QJ_FUSE | QJ_FUSE_GATES)) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    if (flags & ~(QJ_FUSE | QJ_FUSE_GATES | 0xF0u)) return fail(QJ_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    if (fuse_width(flags) > 5) return fail(QJ_ERR_INVALID_ARG, "fusion width %d > 5", fuse_width(flags));
     if (nq < 0) return fail(QJ_ERR_INVALID_ARG, "nq=%d < 0", nq);
     if (nq > 0) {
         if (!out_dev) return fail(QJ_ERR_INVALID_ARG, "out_dev is NULL");
@@ -1575,13 +1585,14 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
             std::rotate(s->plans.begin(), s->plans.begin() + (long)i, s->plans.begin() + (long)i + 1);
         }
     if (!p) {
-        if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, s->n, 2);
+        if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, s->n, fuse_width(flags));
         p = new qj_state_s::CachedPlan;
         p->key.swap(key);
         p->sim = true;
         p->basis = basis;
         p->nq = nq;
         PlanContext ctx{s->n, s->nl, s->g, s->amp_bytes, 1, &s->phys};
+        s->planner.auto_fuse_ = !(flags & QJ_FUSE_GATES);
         s->planner.plan(ctx, gs, true, p->steps);
         p->phys_after = s->phys;
         for (int i = 0; i < nq; ++i) p->qpos[i] = p->phys_after[qubits[i]];
@@ -1726,7 +1737,8 @@ qj_status qj_fuse_circuit(int n, const qj_gate* in, int nin, int max_qubits, qj_
                           int* nout, int* src) {
     if (!nout || (nin > 0 && !in) || (max_out > 0 && (!out || !mats))) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
     if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
-    if (max_qubits < 1 || max_qubits > 2) return fail(QJ_ERR_UNSUPPORTED, "max_qubits must be 1 or 2 (got %d)", max_qubits);
+    if (max_qubits < 1 || max_qubits > 5) return fail(QJ_ERR_UNSUPPORTED, "max_qubits must be in 1..5 (got %d)", max_qubits);
+    const size_t stride = (size_t)2 << (2 * max_qubits);  // 2 * 4^max_qubits doubles per output gate
     qj_state_s tmp;
     tmp.n = n;
     tmp.dt = QJ_C128;
@@ -1753,7 +1765,7 @@ qj_status qj_fuse_circuit(int n, const qj_gate* in, int nin, int max_qubits, qj_
         if (f.src >= 0) {  // a gate copied unchanged
             o.data = in[f.src].data;
         } else {
-            double* m = mats + 32 * i;
+            double* m = mats + stride * i;
             for (size_t j = 0; j < f.data.size(); ++j) {
                 m[2 * j] = f.data[j].real();
                 m[2 * j + 1] = f.data[j].imag();
@@ -1797,6 +1809,7 @@ qj_status qj_plan_circuit(int n, int nshards, int amp_bytes, const qj_gate* gate
     PlanContext ctx{n, n - g, g, amp_bytes, nshards, &map};
     std::vector<Step> steps;
     Planner pl;
+    pl.auto_fuse_ = true;
     pl.plan(ctx, gs, (flags & QJ_FUSE) != 0, steps);
     if ((int)steps.size() > max_steps) return fail(QJ_ERR_CAPACITY, "plan has %zu steps > %d", steps.size(), max_steps);
     for (size_t i = 0; i < steps.size(); ++i) {

@@ -203,6 +203,12 @@ static bool small_enabled() {
     return on;
 }
 
+// QJ_AUTO_FUSE=0 disables the automatic choice of pre-fused tile plans.
+static bool auto_fuse_enabled() {
+    static const bool on = !(getenv("QJ_AUTO_FUSE") && getenv("QJ_AUTO_FUSE")[0] == '0');
+    return on;
+}
+
 void Planner::plan(const PlanContext& ctx, const std::vector<LGate>& gates, bool fuse, std::vector<Step>& out) {
     if (fuse && ctx.nshards == 1 && ctx.n <= small_max_qubits(ctx.amp_bytes) && small_enabled()) {
         std::vector<Step> tmp;
@@ -229,6 +235,29 @@ void Planner::plan(const PlanContext& ctx, const std::vector<LGate>& gates, bool
             }
         }
         flush();
+        return;
+    }
+    if (fuse && auto_fuse_ && auto_fuse_enabled()) {
+        // Window tile passes after the paper's <= 2-qubit gate fusion, or on
+        // the gates as given: keep the plan that moves fewer algorithmic HBM
+        // bytes (dense fused 4x4 matrices absorb 1q gates into their 2q
+        // neighbours -- fewer ops per pass for random circuits -- but turn
+        // diagonal phases into dense work, which QFT-like circuits lose on).
+        std::vector<int> phys_a = *ctx.phys, phys_b = *ctx.phys;
+        PlanContext ca = ctx, cb = ctx;
+        ca.phys = &phys_a;
+        cb.phys = &phys_b;
+        std::vector<Step> a, b;
+        plan_fused(ca, gates, a);
+        plan_fused(cb, fuse_gates(gates, ctx.n, 2), b);
+        auto bytes = [](const std::vector<Step>& v) {
+            double t = 0;
+            for (const Step& st : v) t += st.alg_bytes;
+            return t;
+        };
+        const bool take_b = bytes(b) < 0.9 * bytes(a);
+        *ctx.phys = take_b ? phys_b : phys_a;
+        for (Step& st : take_b ? b : a) out.push_back(std::move(st));
         return;
     }
     if (fuse) {

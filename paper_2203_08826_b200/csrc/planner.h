@@ -47,6 +47,10 @@ struct PlanContext {
 class Planner {
   public:
     void plan(const PlanContext& ctx, const std::vector<LGate>& gates, bool fuse, std::vector<Step>& out);
+    // with fuse: also plan the gates after the paper's <= 2-qubit fusion and
+    // keep the cheaper plan (callers set it when the user asked for no
+    // explicit fusion width; QJ_AUTO_FUSE=0 turns it off)
+    bool auto_fuse_ = false;
 
   private:
     void plan_gate(const PlanContext& ctx, const LGate& g, std::vector<Step>& out);

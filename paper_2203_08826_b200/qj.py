@@ -300,7 +300,8 @@ def fuse_circuit(n, gates, max_qubits=2):
     gates = list(gates)
     arr, ng, keep = pack_gates(gates)
     out = (qj_gate * max(1, ng))()
-    mats = (ctypes.c_double * (32 * max(1, ng)))()
+    stride = 2 * 4 ** max_qubits
+    mats = (ctypes.c_double * (stride * max(1, ng)))()
     cnt = ctypes.c_int()
     src = (ctypes.c_int * max(1, ng))()
     _check(lib().qj_fuse_circuit(n, arr, ng, max_qubits, out, mats, ng, ctypes.byref(cnt), src))
@@ -311,10 +312,18 @@ def fuse_circuit(n, gates, max_qubits=2):
             res.append(gates[src[i]])      # passed through unchanged
         else:
             k = o.nt
-            m = np.array(mats[32 * i:32 * i + 2 * 4 ** k]).view(np.complex128).reshape(2 ** k, 2 ** k)
+            m = np.array(mats[stride * i:stride * i + 2 * 4 ** k]).view(np.complex128).reshape(2 ** k, 2 ** k)
             res.append(FusedGate("dense", o.targets[:o.nt], o.controls[:o.nc], m))
     del keep
     return res
+
+
+def _fuse_gates_flags(fuse_gates):
+    """fuse_gates: False, True (the paper's <= 2-qubit fusion) or a width 1..5."""
+    if not fuse_gates:
+        return 0
+    k = 2 if fuse_gates is True else int(fuse_gates)
+    return QJ_FUSE_GATES | ((k & 15) << 4)
 
 
 class State:
@@ -486,7 +495,7 @@ class State:
         """fuse: window tile passes (QJ_FUSE); fuse_gates: first the paper's
         greedy <= 2-qubit fusion (QJ_FUSE_GATES)."""
         arr, ng, keep = packed if packed is not None else self.pack_circuit(gates)
-        flags = (QJ_FUSE if fuse else 0) | (QJ_FUSE_GATES if fuse_gates else 0)
+        flags = (QJ_FUSE if fuse else 0) | _fuse_gates_flags(fuse_gates)
         _check(lib().qj_apply_circuit(self._h, arr, ng, flags))
         del keep
 
@@ -500,7 +509,7 @@ class State:
         q, nq = _ints(qubits)
         if nq and out is None:
             out = torch.empty(1 << nq, dtype=self.real_dtype, device=self.device)
-        flags = (QJ_FUSE if fuse else 0) | (QJ_FUSE_GATES if fuse_gates else 0)
+        flags = (QJ_FUSE if fuse else 0) | _fuse_gates_flags(fuse_gates)
         _check(lib().qj_simulate(self._h, ctypes.c_uint64(int(basis)), arr, ng, flags, q, nq,
                                  ctypes.c_void_p(out.data_ptr()) if nq else None))
         del keep

@@ -75,3 +75,42 @@ def test_spec_fusion_examples():
     a, b = 0.37, 1.21
     f = Q.fuse_circuit(1, [G.RY(0, a), G.RY(0, b)])
     assert np.max(np.abs(f[0].m - G.RY(0, a + b).matrix())) < 1e-12
+
+
+# ---- wider fusion ("fusing gates up to about five [qubits]
+# may provide additional advantage"): the same greedy rule with max_qubits 1..5
+@pytest.mark.parametrize("k", [1, 3, 4, 5])
+@pytest.mark.parametrize("seed", range(6))
+def test_wide_fusion_equals_original(k, seed):
+    rng = np.random.default_rng(100 * k + seed)
+    n = int(rng.integers(k + 1, 10))
+    circ = C.random_circuit(n, 80, 900 + 10 * k + seed, max_targets=3, max_controls=2)
+    f = Q.fuse_circuit(n, circ.gates, k)
+    assert len(f) <= len(circ)
+    for g in f:  # fused groups never exceed k qubits; wider gates pass through unchanged
+        assert len(g.qubits) <= k or any(g is h for h in circ.gates)
+    psi = rng.standard_normal(2**n) + 1j * rng.standard_normal(2**n)
+    psi /= np.linalg.norm(psi)
+    a = oracle.run(circ, psi)
+    b = oracle.run(C.Circuit(n, f), psi, [g.m if hasattr(g, "m") else g.matrix() for g in f])
+    assert np.max(np.abs(a - b)) < 1e-12
+
+
+def test_wide_fusion_counts_monotone_and_generators():
+    """Wider fusion never yields more gates than narrower on the BASELINE
+    generators, k=2 reproduces Table 2, and every width computes the same state."""
+    for circ in (C.qft(10), C.bv(10), C.supremacy(3, 4, 8), C.qaoa(10, 2), C.variational(10, layers=2)):
+        n = circ.n
+        counts = [len(Q.fuse_circuit(n, circ.gates, k)) for k in (1, 2, 3, 4, 5)]
+        assert counts[1:] == sorted(counts[1:], reverse=True), (circ.name, counts)
+        psi = oracle.basis_state(n, 3)
+        a = oracle.run(circ, psi)
+        for k in (3, 5):
+            f = Q.fuse_circuit(n, circ.gates, k)
+            b = oracle.run(C.Circuit(n, f), psi, [g.m if hasattr(g, "m") else g.matrix() for g in f])
+            assert np.max(np.abs(a - b)) < 1e-12, (circ.name, k)
+
+
+def test_fusion_width_rejected_above_5():
+    with pytest.raises(Q.QJError):
+        Q.fuse_circuit(3, [G.H(0)], 6)

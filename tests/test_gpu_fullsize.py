@@ -339,3 +339,27 @@ def test_simulate_repeated_window_single_tile(dt):
     assert err <= TOL[dt], f"max abs err {err:.3e}"
     assert np.max(np.abs(p.cpu().numpy() - oracle.probabilities(exp, n, [4, 15]))) <= TOL[dt]
     assert st.counters()["launches"] > 0
+
+
+# ------------------------------------------------ wider gate fusion (QJ_FUSE_GATES_K)
+@pytest.mark.parametrize("dt", [np.complex128, np.complex64], ids=["c128", "c64"])
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+@pytest.mark.parametrize("fuse", [False, True], ids=["passes", "tiles"])
+def test_fuse_gates_width_vs_oracle(dt, k, fuse):
+    """Greedy fusion into <= k-qubit dense gates
+    followed by per-gate passes or window tile passes: every amplitude
+    against the oracle on the unfused circuit (n = 16: several tiles)."""
+    n = 16
+    circ = C.supremacy(4, 4, 8)
+    circ.gates += C.random_circuit(n, 60, 77 + k, max_targets=2, max_controls=1).gates
+    rng = np.random.default_rng(k)
+    v = rng.standard_normal(2**n) + 1j * rng.standard_normal(2**n)
+    psi = (v / np.linalg.norm(v)).astype(dt)
+    exp = oracle.run(circ, psi.astype(np.complex128), [g.matrix().astype(dt).astype(np.complex128) for g in circ.gates])
+    x = torch.from_numpy(psi.copy()).cuda()
+    st = qjp.State(x, basis=None)
+    st.apply_circuit(circ.gates, fuse=fuse, fuse_gates=k)
+    st.canonicalize()
+    st.sync()
+    err = np.max(np.abs(x.cpu().numpy().astype(np.complex128) - exp))
+    assert err <= TOL[dt], f"max abs err {err:.3e}"

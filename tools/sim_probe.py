@@ -22,14 +22,17 @@ pb = torch.empty(1024, dtype=st.real_dtype, device="cuda")
 q = list(range(10))
 
 
+FG = int(os.environ.get("QJ_PROBE_FG", "0"))  # gate-fusion width before tiling (0 = none)
+
+
 def sep():
     st.reset(x)
-    st.apply_circuit(None, fuse=True, packed=packed)
+    st.apply_circuit(None, fuse=True, packed=packed, fuse_gates=FG)
     st.probabilities(q, out=pb)
 
 
 def sim():
-    st.simulate(x, qubits=q, packed=packed, out=pb)
+    st.simulate(x, qubits=q, packed=packed, out=pb, fuse_gates=FG)
 
 
 res = {}
