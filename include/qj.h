@@ -389,6 +389,15 @@ qj_status qj_plan_circuit(int n, int nshards, int amp_bytes, const qj_gate* gate
 qj_status qj_plan_canonicalize(int n, int nshards, const int* phys_in, qj_plan_step* out, int max_steps,
                                int* nsteps);
 
+/* Tooling (host only, no GPU): plan the circuit with QJ_FUSE on one shard of
+ * n qubits (amp_bytes 16 = complex128, 8 = complex64), emit the source of
+ * every tile-pass kernel the JIT would compile (written as dir/qj_tile_K.cu
+ * when dir != NULL) and, with compile != 0, compile each with NVRTC for
+ * sm_100a.  *nkernels receives the number of tile passes.  Errors: as
+ * qj_plan_circuit; UNSUPPORTED with the NVRTC log on a compile failure. */
+qj_status qj_debug_tile_sources(int n, int amp_bytes, const qj_gate* gates, int ngates, uint32_t flags,
+                                const char* dir, int compile, int* nkernels);
+
 /* The paper's gate fusion (Table 2 Gates* / Depth*), host
  * only: greedily combine the circuit into gates of at most `max_qubits` (1 to
  * 5; the paper's fusion is 2) qubits.  Fused groups come back as

@@ -1943,6 +1943,43 @@ qj_status qj_plan_canonicalize(int n, int nshards, const int* phys_in, qj_plan_s
     return QJ_OK;
 }
 
+qj_status qj_debug_tile_sources(int n, int amp_bytes, const qj_gate* gates, int ngates, uint32_t flags,
+                                const char* dir, int compile, int* nkernels) {
+    if (!nkernels || (ngates > 0 && !gates)) return fail(QJ_ERR_INVALID_ARG, "NULL argument");
+    if (amp_bytes != 8 && amp_bytes != 16) return fail(QJ_ERR_DTYPE, "amp_bytes must be 8 or 16");
+    if (n < 1 || n > QJ_MAX_QUBITS) return fail(QJ_ERR_CAPACITY, "n=%d outside [1,%d]", n, QJ_MAX_QUBITS);
+    qj_state_s tmp;
+    tmp.n = n;
+    tmp.dt = amp_bytes == 16 ? QJ_C128 : QJ_C64;
+    std::vector<LGate> gs((size_t)ngates);
+    for (int i = 0; i < ngates; ++i) {
+        const qj_gate& q = gates[i];
+        if (q.nt > QJ_MAX_TARGETS || q.nc > QJ_MAX_CONTROLS)
+            return fail(QJ_ERR_TOO_MANY_TARGETS, "gate %d: nt=%d nc=%d exceeds the limits", i, q.nt, q.nc);
+        if (qj_status st = make_lgate(&tmp, q.kind, q.targets, q.nt, q.controls, q.nc, q.data, gs[(size_t)i])) return st;
+    }
+    if (flags & QJ_FUSE_GATES) gs = fuse_gates(gs, n, fuse_width(flags));
+    std::vector<int> map(n);
+    for (int q = 0; q < n; ++q) map[q] = n - 1 - q;
+    PlanContext ctx{n, n, 0, amp_bytes, 1, &map};
+    std::vector<Step> steps;
+    Planner pl;
+    pl.auto_fuse_ = !(flags & QJ_FUSE_GATES);
+    pl.plan(ctx, gs, true, steps);
+    int k = 0;
+    for (const Step& st : steps) {
+        if (st.type != Step::TILE) continue;
+        std::string path = dir ? std::string(dir) + "/qj_tile_" + std::to_string(k) + ".cu" : std::string();
+        std::string err;
+        const bool ok = amp_bytes == 16 ? tile_jit_debug_source<double>(st.tile, n, dir ? path.c_str() : nullptr, compile != 0, &err)
+                                        : tile_jit_debug_source<float>(st.tile, n, dir ? path.c_str() : nullptr, compile != 0, &err);
+        if (!ok) return fail(QJ_ERR_UNSUPPORTED, "tile pass %d: %s", k, err.c_str());
+        ++k;
+    }
+    *nkernels = k;
+    return QJ_OK;
+}
+
 qj_status qj_sync(qj_state s) {
     if (!s) return fail(QJ_ERR_INVALID_ARG, "state is NULL");
     cudaError_t e = cudaStreamSynchronize(s->stream);

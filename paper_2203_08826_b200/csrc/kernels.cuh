@@ -35,6 +35,7 @@
 #include <unordered_map>
 
 #include "common.cuh"
+#include "dense_tc.h"
 #include "qj_internal.h"
 
 namespace qj {
@@ -896,6 +897,9 @@ cudaError_t run_pass(const Pass& p, void* psi, int nl, cudaStream_t st, void* sc
             return launch_diag<R>(p, psi, nl, st, ls);
         default:
             if (p.k > 5) return launch_bigk<R>(p, psi, nl, st, scratch, scratch_bytes, ls);
+            if constexpr (sizeof(R) == 4) {  // complex64 5-qubit blocks: tensor cores (dense_tc.cu)
+                if (dense_tc_enabled() && dense_tc_supports(p, nl)) return run_dense_tc(p, psi, nl, st, ls);
+            }
             return launch_gate<R>(p, psi, nl, st, ls);
     }
 }

@@ -32,6 +32,7 @@
 
 #include <stdint.h>
 
+#include <string>
 #include <vector>
 
 #include "qj_internal.h"
@@ -98,12 +99,24 @@ struct PreparedTile {
     void* jit = nullptr;              // JIT function or nullptr (interpreter)
     size_t smem = 0;
     unsigned grid = 0;
+    int threads = TILE_THREADS;  // block size (JIT ring form: 2 x TILE_THREADS)
     int amp_bytes = 16;
 };
 template <typename R>
 cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out);
 cudaError_t tile_launch_prepared(const PreparedTile& p, cudaStream_t st, LaunchStats& ls);
 void tile_release(PreparedTile& p);
+
+// Host lowering of a planned pass into kernel parameters + program buffer
+// (false when it exceeds a capacity).
+template <typename R>
+bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned char>& blob);
+
+// Tooling (qj_debug_tile_sources): write the JIT source of a lowered pass to
+// `path` and, with `compile`, compile it with NVRTC for sm_100a (no GPU
+// needed); returns false with *err set on a lowering or compile failure.
+template <typename R>
+bool tile_jit_debug_source(const TileSpec& t, int nl, const char* path, bool compile, std::string* err);
 
 // Whether a planned pass lowers within the kernel's capacities.
 bool tile_fits(const TileSpec& t, int nl, int amp_bytes);

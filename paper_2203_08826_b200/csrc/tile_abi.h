@@ -103,8 +103,23 @@ struct TileTablesLayout {
     uint32_t terms, slots, mats, fac;
 };
 
+// Ring form (JIT): the tile as a TMA box of a <= 5-D view of the state
+// (doubles; dim 0 = the window's low contiguous bits x amplitude, then
+// alternating window segments (box = extent, <= 256) and gap segments (box 1,
+// the tile's coordinate)); smem receives the tile in window-local order.
+struct TmapGeom {
+    int rank = 0;
+    uint64_t extent[5] = {};
+    uint64_t stride_bytes[5] = {};  // [0] unused (contiguous)
+    uint32_t box[5] = {};
+    int start_bit[5] = {};          // amplitude-index bit where the dim starts
+    int len[5] = {};                // its bits (dim 0: amplitude bits only)
+    bool gap[5] = {};
+};
+
 template <typename R>
 struct TileArgs {
+    alignas(64) unsigned char tmap[128];  // CUtensorMap of the ring form's TMA loads (JIT ring kernels only)
     void* psi;
     const unsigned char* tables;  // device program buffer of this pass
     TileTablesLayout lay;

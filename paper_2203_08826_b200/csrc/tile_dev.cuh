@@ -527,6 +527,47 @@ __device__ __forceinline__ void cp_amp<float>(Cx<float>* s, const Cx<float>* g) 
     cp_async8(s, g);
 }
 
+// ---------------------------------------------------------------- ring form (TMA)
+// JIT kernels in the ring form run two workers (256 threads each) per CTA over
+// a ring of tile buffers filled by bulk asynchronous copies (TMA engine,
+// cp.async.bulk) that complete on one mbarrier per buffer; a worker
+// synchronises its own 256 threads with a named barrier.
+__device__ __forceinline__ void worker_sync(int wk) {
+    asm volatile("bar.sync %0, 256;\n" ::"r"(1 + wk) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// generic-proxy accesses of a buffer before the async proxy (TMA) writes it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// global -> shared bulk copy (16-byte multiple), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <typename R>
 __device__ __forceinline__ void tile_prefetch(const TileArgs<R>& a, uint64_t tile, Cx<R>* sm, int tid) {
     tile_prefetch_issue(a, tile, sm, tid);

@@ -21,7 +21,13 @@ struct JitKernel {
     int npt = 0;
     size_t smem_extra = 0;
     int blocks = 2;  // resident CTAs per SM it was compiled for (grid = SMs x blocks)
+    int threads = TILE_THREADS;  // block size (ring form: two workers)
+    bool tmap = false;           // ring form with TMA tensor loads: TileArgs::tmap must be encoded
 };
+
+// Encode the ring form's tensor map (TileArgs::tmap) for a->psi.
+template <typename R>
+cudaError_t tile_jit_encode_tmap(TileArgs<R>* a);
 
 // The specialised kernel for this lowered pass (compiled and cached on first
 // use; `blob` is the host copy of the pass's program buffer), or nullptr with
@@ -37,6 +43,7 @@ void tile_jit_fill(const JitKernel& k, TileArgs<R>* a, const unsigned char* blob
 // Whether JIT kernels can be built here (NVRTC + driver found, QJ_JIT != 0).
 bool tile_jit_available();
 
-cudaError_t tile_jit_launch(void* f, const void* args, unsigned grid, size_t smem, cudaStream_t st);
+cudaError_t tile_jit_launch(void* f, const void* args, unsigned grid, size_t smem, cudaStream_t st,
+                            int threads = TILE_THREADS);
 
 }  // namespace qj

@@ -529,8 +529,12 @@ cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, Tile
     const JitKernel* jk = tile_jit_kernel<R>(*a, blob.empty() ? nullptr : blob.data(), &jerr, nullptr);
     if (jk) {
         tile_jit_fill<R>(*jk, a, blob.data());
+        if (jk->tmap) {
+            e = tile_jit_encode_tmap<R>(a);
+            if (e != cudaSuccess) return e;
+        }
         const uint64_t jgrid = std::min<uint64_t>(a->ntiles, (uint64_t)sms * jk->blocks);
-        e = tile_jit_launch(jk->f, a, (unsigned)jgrid, smem + jk->smem_extra, st);
+        e = tile_jit_launch(jk->f, a, (unsigned)jgrid, smem + jk->smem_extra, st, jk->threads);
     } else {
         static bool warned = false;
         if (!warned && getenv("QJ_DEBUG_JIT")) fprintf(stderr, "[qj jit] interpreter fallback: %s\n", jerr.c_str());
@@ -571,8 +575,13 @@ cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out
     out.jit = jk ? jk->f : nullptr;
     if (jk) {
         tile_jit_fill<R>(*jk, a, blob.data());
+        if (jk->tmap) {
+            cudaError_t e = tile_jit_encode_tmap<R>(a);
+            if (e != cudaSuccess) return e;
+        }
         out.smem += jk->smem_extra;
         out.grid = (unsigned)std::min<uint64_t>(a->ntiles, (uint64_t)sms * jk->blocks);
+        out.threads = jk->threads;
     }
     out.args.assign(reinterpret_cast<unsigned char*>(a), reinterpret_cast<unsigned char*>(a) + sizeof(TileArgs<R>));
     return cudaSuccess;
@@ -581,7 +590,7 @@ cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out
 cudaError_t tile_launch_prepared(const PreparedTile& p, cudaStream_t st, LaunchStats& ls) {
     cudaError_t e;
     if (p.jit) {
-        e = tile_jit_launch(p.jit, p.args.data(), p.grid, p.smem, st);
+        e = tile_jit_launch(p.jit, p.args.data(), p.grid, p.smem, st, p.threads);
     } else if (p.amp_bytes == 16) {
         tile_kernel<double><<<p.grid, TILE_THREADS, p.smem, st>>>(*reinterpret_cast<const TileArgs<double>*>(p.args.data()));
         e = cudaGetLastError();
@@ -598,6 +607,8 @@ void tile_release(PreparedTile& p) {
     p.dev = nullptr;
 }
 
+template bool lower_tile<float>(const TileSpec&, int, TileArgs<float>*, std::vector<unsigned char>&);
+template bool lower_tile<double>(const TileSpec&, int, TileArgs<double>*, std::vector<unsigned char>&);
 template cudaError_t tile_prepare<float>(const TileSpec&, void*, int, PreparedTile&);
 template cudaError_t tile_prepare<double>(const TileSpec&, void*, int, PreparedTile&);
 template cudaError_t run_tile<float>(const TileSpec&, void*, int, cudaStream_t, TileStaging&, LaunchStats&);

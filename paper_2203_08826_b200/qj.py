@@ -37,7 +37,7 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
            "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit", "qj_collapse",
            "qj_sample_distribution", "qj_sample", "qj_measure", "qj_state_init_host",
-           "qj_simulate", "qj_state_layout", "qj_plan_canonicalize"]
+           "qj_simulate", "qj_state_layout", "qj_plan_canonicalize", "qj_debug_tile_sources"]
 
 
 class QJError(RuntimeError):
@@ -122,6 +122,7 @@ def lib():
                              IP, IP], S),
         "qj_exchange_peer": ([I, I, IP, IP], None),
         "qj_plan_canonicalize": ([I, I, IP, ctypes.POINTER(qj_plan_step), I, IP], S),
+        "qj_debug_tile_sources": ([I, I, ctypes.POINTER(qj_gate), I, ctypes.c_uint32, ctypes.c_char_p, I, IP], S),
         "qj_fuse_circuit": ([I, ctypes.POINTER(qj_gate), I, I, ctypes.POINTER(qj_gate), ctypes.POINTER(ctypes.c_double),
                              I, IP, IP], S),
         "qj_collapse": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_double)], S),
@@ -266,6 +267,17 @@ def plan_circuit(n, nshards, gates, fuse=False, amp_bytes=16, max_steps=1 << 16)
                       "fix": [(o.fpos[j], o.fval[j]) for j in range(o.nfix)], "touch": o.touch, "m": m,
                       "gbit": o.gbit, "lbit": o.lbit, "alg_bytes": o.alg_bytes})
     return steps, list(phys)
+
+
+def debug_tile_sources(n, gates, amp_bytes=16, out_dir=None, compile=True, fuse_gates=False):
+    """Generate (and NVRTC-compile, no GPU needed) every JIT tile kernel of the
+    fused plan; returns the number of tile passes."""
+    arr, ng, keep = pack_gates(gates)
+    cnt = ctypes.c_int()
+    _check(lib().qj_debug_tile_sources(n, amp_bytes, arr, ng, _fuse_gates_flags(fuse_gates),
+                                       out_dir.encode() if out_dir else None, 1 if compile else 0, ctypes.byref(cnt)))
+    del keep
+    return cnt.value
 
 
 def plan_canonicalize(n, nshards, phys, max_steps=4096):

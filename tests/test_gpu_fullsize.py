@@ -363,3 +363,37 @@ def test_fuse_gates_width_vs_oracle(dt, k, fuse):
     st.sync()
     err = np.max(np.abs(x.cpu().numpy().astype(np.complex128) - exp))
     assert err <= TOL[dt], f"max abs err {err:.3e}"
+
+
+# ------------------------------------------------ complex64 5-qubit dense passes on the tensor cores
+@pytest.mark.parametrize("n", [12, 14, 20])
+def test_dense5_c64_tensor_core_pass(n):
+    """Dense 5-qubit gates on complex64 states run as 3xTF32 tcgen05.mma
+    contractions (dense_tc.cu): targets on high, low and mixed bits, unsorted
+    listed order, with and without controls, against the oracle (R8 1e-5)."""
+    rng = np.random.default_rng(500 + n)
+    v = rng.standard_normal(2**n) + 1j * rng.standard_normal(2**n)
+    psi = (v / np.linalg.norm(v)).astype(np.complex64)
+    circ = C.Circuit(n, name="dense5")
+    sets = [tuple(range(n - 5, n)), tuple(range(5)), (0, n - 1, 3, n // 2, 7)]
+    for _ in range(5):
+        sets.append(tuple(int(q) for q in rng.permutation(n)[:5]))
+    for i, ts in enumerate(sets):
+        rest = [q for q in range(n) if q not in ts]
+        ctrls = tuple(int(q) for q in rng.permutation(rest)[: i % 3]) if n >= 14 else ()
+        circ.append(G.unitary("U5", ts, G.random_unitary(5, rng), ctrls))
+    mats = [g.matrix().astype(np.complex64).astype(np.complex128) for g in circ.gates]
+    exp = oracle.run(circ, psi.astype(np.complex128), mats)
+    x = torch.from_numpy(psi.copy()).cuda()
+    st = qjp.State(x, basis=None)
+    for g in circ.gates:
+        st.apply_gate(g.targets, g.data[0], g.controls)
+    st.sync()
+    err = np.max(np.abs(x.cpu().numpy().astype(np.complex128) - exp))
+    assert err <= 1e-5, f"max abs err {err:.3e}"
+    # and the same gates as a fused circuit at width 5 (QJ_FUSE_GATES_K(5))
+    x2 = torch.from_numpy(psi.copy()).cuda()
+    s2 = qjp.State(x2, basis=None)
+    s2.apply_circuit(circ.gates, fuse_gates=5)
+    s2.sync()
+    assert np.max(np.abs(x2.cpu().numpy().astype(np.complex128) - exp)) <= 1e-5
