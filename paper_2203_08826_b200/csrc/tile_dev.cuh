@@ -86,6 +86,72 @@ __device__ __forceinline__ void op_u1(Cx<R> (&v)[TILE_NREG], const Cx<R>* m, uin
     }
 }
 
+// cfma with the matrix entry's zero components known at compile time
+// (NZ bit 0: re != 0, bit 1: im != 0); JIT kernels specialise U1 / U2 ops on
+// the zero pattern of their matrices (RX / RY / fSim are half zeros), the
+// values stay runtime data.  Same FMA order as cfma on the nonzero terms.
+template <typename R, int NZ>
+__device__ __forceinline__ void cfma_nz(Cx<R>& acc, Cx<R> a, Cx<R> b) {
+    if constexpr (NZ & 1) acc.re = fma(a.re, b.re, acc.re);
+    if constexpr (NZ & 2) acc.re = fma(-a.im, b.im, acc.re);
+    if constexpr (NZ & 1) acc.im = fma(a.re, b.im, acc.im);
+    if constexpr (NZ & 2) acc.im = fma(a.im, b.re, acc.im);
+}
+
+template <typename R, int A, bool C, uint32_t NZ>
+__device__ __forceinline__ void op_u1_nz(Cx<R> (&v)[TILE_NREG], const Cx<R>* m, uint32_t crm, uint32_t crv, bool ok) {
+    const Cx<R> m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+#pragma unroll
+    for (int j = 0; j < TILE_NREG / 2; ++j) {
+        const int lo = ((j >> A) << (A + 1)) | (j & ((1 << A) - 1));
+        const int hi = lo | (1 << A);
+        if (!C || (ok && ((uint32_t)lo & crm) == crv)) {
+            const Cx<R> x = v[lo], y = v[hi];
+            Cx<R> o0{R(0), R(0)}, o1{R(0), R(0)};
+            cfma_nz<R, (NZ >> 0) & 3>(o0, m00, x);
+            cfma_nz<R, (NZ >> 2) & 3>(o0, m01, y);
+            cfma_nz<R, (NZ >> 4) & 3>(o1, m10, x);
+            cfma_nz<R, (NZ >> 6) & 3>(o1, m11, y);
+            v[lo] = o0;
+            v[hi] = o1;
+        }
+    }
+}
+
+// 4x4 on register bits A (matrix MSB) and B, zero pattern NZ (2 bits per entry, row-major)
+template <typename R, int A, int B, bool C, uint32_t NZ>
+__device__ __forceinline__ void op_u2_nz(Cx<R> (&v)[TILE_NREG], const Cx<R>* m, uint32_t crm, uint32_t crv, bool ok) {
+    constexpr int LO = A < B ? A : B, HI = A < B ? B : A;
+#pragma unroll
+    for (int j = 0; j < TILE_NREG / 4; ++j) {
+        int base = ((j >> LO) << (LO + 1)) | (j & ((1 << LO) - 1));
+        base = ((base >> HI) << (HI + 1)) | (base & ((1 << HI) - 1));
+        if (C && !(ok && ((uint32_t)base & crm) == crv)) continue;
+        int id[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) id[q] = base | (((q >> 1) & 1) << A) | ((q & 1) << B);
+        Cx<R> in[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) in[q] = v[id[q]];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            Cx<R> o{R(0), R(0)};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                constexpr uint32_t dummy = 0;
+                (void)dummy;
+                switch ((NZ >> (2 * (r * 4 + c))) & 3) {
+                    case 1: cfma_nz<R, 1>(o, m[r * 4 + c], in[c]); break;
+                    case 2: cfma_nz<R, 2>(o, m[r * 4 + c], in[c]); break;
+                    case 3: cfma_nz<R, 3>(o, m[r * 4 + c], in[c]); break;
+                    default: break;
+                }
+            }
+            v[id[r]] = o;
+        }
+    }
+}
+
 template <typename R, int A, bool C>
 __device__ __forceinline__ void op_x(Cx<R> (&v)[TILE_NREG], uint32_t crm, uint32_t crv, bool ok) {
 #pragma unroll

@@ -59,15 +59,22 @@ struct PassBuild {
 // phase run before a non-diagonal op adds ~1 complex multiply), used to keep a
 // pass's compute within its HBM time.
 double op_cost(const HOp& op) {
+    // dense U1 / U2: 2 FMAs per output amplitude per nonzero matrix component
+    // (the JIT kernels skip zero real / imaginary parts: RX, RY, fSim)
+    auto nzc = [&](int count) {
+        double c = 0;
+        for (int e = 0; e < count; ++e) c += (op.m[e].real() != 0) + (op.m[e].imag() != 0);
+        return c;
+    };
     switch (op.type) {
         case TO_X:
         case TO_SWAP: return 1 + 4;
-        case TO_U2: return 16 + 4;
+        case TO_U2: return nzc(16) / 2 + 4;
         default: break;
     }
     const bool h = op.m.size() == 4 && op.cmask == 0 && op.m[0] == op.m[1] && op.m[0] == op.m[2] &&
                    op.m[3] == -op.m[0] && op.m[0].imag() == 0;
-    return h ? 2 + 4 : 8 + 4;
+    return h ? 2 + 4 : nzc(4) + 4;
 }
 
 // Phase terms of a diagonal gate on physical positions.

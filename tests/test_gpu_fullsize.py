@@ -375,7 +375,7 @@ def test_dense5_c64_tensor_core_pass(n):
     v = rng.standard_normal(2**n) + 1j * rng.standard_normal(2**n)
     psi = (v / np.linalg.norm(v)).astype(np.complex64)
     circ = C.Circuit(n, name="dense5")
-    sets = [tuple(range(n - 5, n)), tuple(range(5)), (0, n - 1, 3, n // 2, 7)]
+    sets = [tuple(range(n - 5, n)), tuple(range(5)), (0, n - 1, 3, n // 2, 5)]
     for _ in range(5):
         sets.append(tuple(int(q) for q in rng.permutation(n)[:5]))
     for i, ts in enumerate(sets):
