@@ -367,6 +367,12 @@ __global__ void __launch_bounds__(kThreads) diag_kernel(const __grid_constant__ 
         wact[w] = ((lowlane | w) & a.low_mask) == a.low_val;
         any |= wact[w];
     }
+    // fixed bits among the lowest ones leave 32-byte sectors half used: a lane
+    // whose sector partner (lane ^ 1) is active loads and stores its 16 bytes
+    // unchanged too, so DRAM sees whole-sector writes (a partial-sector write
+    // is a read-modify-write under ECC).  Measured per-pass sweep: CU1 / CZ on
+    // bits (0,1) at 0.21 of HBM before.
+    const bool io = any || __shfl_xor_sync(0xffffffffu, any, 1);
     Vec* psi = reinterpret_cast<Vec*>(a.psi);
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -378,11 +384,11 @@ __global__ void __launch_bounds__(kThreads) diag_kernel(const __grid_constant__ 
         for (int uu = 0; uu < U; ++uu) {
             const uint64_t u = u0 + uu;
             base[uu] = unit_base(u, LB, a.nins, a.ins_pos, a.fix_val) | lowlane;
-            v[uu] = (u < a.units && any) ? ldv(psi + (base[uu] >> V)) : zv;
+            v[uu] = (u < a.units && io) ? ldv(psi + (base[uu] >> V)) : zv;
         }
 #pragma unroll
         for (int uu = 0; uu < U; ++uu) {
-            if (u0 + uu >= a.units || !any) continue;
+            if (u0 + uu >= a.units || !io) continue;
             Cx<R> amp[NW];
             unpack(v[uu], amp);
 #pragma unroll
