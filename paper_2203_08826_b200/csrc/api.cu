@@ -1986,6 +1986,7 @@ qj_status qj_sync(qj_state s) {
     if (e != cudaSuccess) return cuda_fail(e, "qj_sync");
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "qj_sync");
+    if (tile_check_failed()) return fail(QJ_ERR_CUDA, "qj_sync: a checked tile kernel (QJ_JIT_CHECK=1) caught an out-of-bounds access");
     return QJ_OK;
 }
 

@@ -593,6 +593,15 @@ __device__ __forceinline__ void cp_amp<float>(Cx<float>* s, const Cx<float>* g) 
     cp_async8(s, g);
 }
 
+// Bounds check of a global amplitude pointer (checked JIT kernels only).
+template <typename R>
+__device__ __forceinline__ bool qj_chk(const TileArgs<R>& a, const Cx<R>* p, uint64_t count = 1) {
+    const uint64_t off = (uint64_t)(p - reinterpret_cast<const Cx<R>*>(a.psi));
+    if (off < a.namps && count <= a.namps - off) return true;
+    if (a.chk) atomicOr(a.chk, 1u);
+    return false;
+}
+
 // ---------------------------------------------------------------- ring form (TMA)
 // JIT kernels in the ring form run two workers (256 threads each) per CTA over
 // a ring of tile buffers filled by bulk asynchronous copies (TMA engine,

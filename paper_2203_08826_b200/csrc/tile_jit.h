@@ -25,6 +25,11 @@ struct JitKernel {
     bool tmap = false;           // ring form with TMA tensor loads: TileArgs::tmap must be encoded
 };
 
+// Checked JIT kernels (QJ_JIT_CHECK=1): the device flag their bounds checks
+// set (nullptr when off), and whether it was set since the last call (resets it).
+unsigned int* tile_check_flag();
+bool tile_check_failed();
+
 // Encode the ring form's tensor map (TileArgs::tmap) for a->psi.
 template <typename R>
 cudaError_t tile_jit_encode_tmap(TileArgs<R>* a);

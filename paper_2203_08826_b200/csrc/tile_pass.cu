@@ -73,6 +73,8 @@ bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned 
     std::memset(a, 0, sizeof(TileArgs<R>));
     if ((int)t.segs.size() < 1 || (int)t.segs.size() > TILE_MAXSEG) return false;
     a->ntiles = 1ull << (nl - TILE_W - __builtin_popcountll(t.fix_mask));
+    a->namps = 1ull << nl;
+    a->chk = tile_check_flag();
     a->gbase = t.gbase;
     a->synth = t.synth_index;
     a->fixmask = t.fix_mask;

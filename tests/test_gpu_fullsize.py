@@ -397,3 +397,21 @@ def test_dense5_c64_tensor_core_pass(n):
     s2.apply_circuit(circ.gates, fuse_gates=5)
     s2.sync()
     assert np.max(np.abs(x2.cpu().numpy().astype(np.complex128) - exp)) <= 1e-5
+
+
+# ------------------------------------------------ bounds-checked JIT kernels (QJ_JIT_CHECK=1)
+def test_checked_tile_kernels_subprocess():
+    """compute-sanitizer is closed on this pool, so the JIT tile kernels carry
+    their own bounds checks when QJ_JIT_CHECK=1 (every global load / store /
+    bulk copy checked against the state size; a violation sets a device flag
+    that qj_sync reports instead of touching memory).  Run every tile-kernel
+    form -- two-CTA, CTA pair, ring (TMA), live tile, synthesised pass, fused
+    marginal, complex64 -- in a fresh process with the checks compiled in."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QJ_JIT_CHECK="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_driver.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "sanitize driver done" in r.stdout

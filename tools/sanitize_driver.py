@@ -1,5 +1,6 @@
-"""Small invocations of every kernel family for compute-sanitizer runs
-(memcheck / racecheck): per-gate passes, the whole-state SMEM program, JIT
+"""Small invocations of every kernel family -- for compute-sanitizer runs
+(closed on this pool) and for the bounds-checked JIT mode (QJ_JIT_CHECK=1,
+tests/test_gpu_fullsize.py::test_checked_tile_kernels_subprocess): per-gate passes, the whole-state SMEM program, JIT
 tile passes in the two-CTA, CTA-pair, live-tile and ring (TMA) forms, the
 tensor-core dense pass, readout and measurement.  Each result is checked
 against the oracle so a silent corruption fails the run too."""
@@ -60,6 +61,23 @@ st.sync()
 e, _ = oracle.qft_basis_maxerr(t.cpu().numpy(), n, 12345)
 assert e < 1e-12
 print("ok ring qft20", e, flush=True)
+# complex64 fused random circuit over several tiles, and a sharded fused run
+sc = C.supremacy(4, 5, 8)
+exp = oracle.run(sc, oracle.basis_state(sc.n, 0), [g.matrix().astype(np.complex64).astype(np.complex128) for g in sc.gates])
+t = torch.empty(2**sc.n, dtype=torch.complex64, device=dev)
+st = qj.State(t, basis=0)
+st.apply_circuit(sc.gates, fuse=True)
+st.canonicalize()
+st.sync()
+check(t, exp, 1e-5, "supremacy20 c64 fused")
+shards = [torch.empty(2**18, dtype=torch.complex128, device=dev) for _ in range(4)]
+sh = qj.State.sharded(shards, 20, basis=12345)
+sh.apply_circuit(C.qft(20).gates, fuse=True)
+sh.canonicalize()
+sh.sync()
+e, _ = oracle.qft_basis_maxerr(torch.cat(shards).cpu().numpy(), 20, 12345)
+assert e < 1e-12
+print("ok sharded qft20", e, flush=True)
 # tensor-core dense 5-qubit pass (complex64, n = 12)
 rng = np.random.default_rng(1)
 psi = rng.standard_normal(2**12) + 1j * rng.standard_normal(2**12)
