@@ -367,12 +367,10 @@ __global__ void __launch_bounds__(kThreads) diag_kernel(const __grid_constant__ 
         wact[w] = ((lowlane | w) & a.low_mask) == a.low_val;
         any |= wact[w];
     }
-    // fixed bits among the lowest ones leave 32-byte sectors half used: a lane
-    // whose sector partner (lane ^ 1) is active loads and stores its 16 bytes
-    // unchanged too, so DRAM sees whole-sector writes (a partial-sector write
-    // is a read-modify-write under ECC).  Measured per-pass sweep: CU1 / CZ on
-    // bits (0,1) at 0.21 of HBM before.
-    const bool io = any || __shfl_xor_sync(0xffffffffu, any, 1);
+    // (tried: lanes whose 32-byte sector partner is active also load and store
+    // unchanged data, for whole-sector writes -- measured slower for CU1 on
+    // bits (0,1) / (0,29), 6.5 -> 7.0 / 3.9 -> 5.0 ms; only touched vectors move)
+    const bool io = any;
     Vec* psi = reinterpret_cast<Vec*>(a.psi);
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
