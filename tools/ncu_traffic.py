@@ -42,7 +42,7 @@ def main():
         per[(row["ID"], row["Kernel Name"])][row["Metric Name"]] = (float(row["Metric Value"].replace(",", "")),
                                                                     row["Metric Unit"])
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-             "msecond": 1e-3, "second": 1}
+             "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
     agg = collections.defaultdict(lambda: {"dram": 0.0, "ms": 0.0, "launches": 0})
     for (_, name), met in per.items():
         k = kind_of(name)
