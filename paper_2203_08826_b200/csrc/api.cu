@@ -1645,7 +1645,9 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
                 for (int j = 0; j < TILE_W; ++j) w |= p->steps.back().tile.wpos[j] == p->qpos[i];
                 in_window &= w;
             }
-        if (nq > 0 && last_tile && in_window) {  // bins depend on (thread, register) only
+        // bins depend on (thread, register) only when every readout bit is in the
+        // last window; otherwise on the tile too (per-CTA SMEM bins, nq <= 10)
+        if (nq > 0 && last_tile && (in_window || nq <= 10)) {
             Step& l = p->steps.back();
             l.tile.nbins_q = nq;
             for (int i = 0; i < nq; ++i) l.tile.bin_pos[i] = (int8_t)p->qpos[i];
