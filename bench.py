@@ -194,24 +194,39 @@ def oracle_time(wl, threads=0, budget_s=30.0):
             sample = (f"whole circuit ({len(gates)} gates) from |basis>" if not extra else
                       f"first {done} of {len(gates)} gates from |basis>, extrapolated by gate count")
         else:
-            classes = {}
-            for g in gates:
-                key = (len(g.targets), len(g.controls))
-                classes.setdefault(key, [g, 0])
-                classes[key][1] += 1
-            value, parts = 0.0, []
-            for key, (g, cnt) in sorted(classes.items()):
-                t0 = time.perf_counter()
-                oracle.apply_matrix(psi, out, n, g.targets, g.controls, g.matrix())
-                dt = time.perf_counter() - t0
-                value += dt * cnt
-                parts.append(f"{cnt}x[{key[0]}t,{key[1]}c] {dt:.3f}s")
+            per = oracle_class_times(psi, out, n, gates)
+            counts = class_counts(gates)
+            value = sum(per[k] * c for k, c in counts.items())
             extra = True
-            sample = f"one gate per class on a 2^{n} state, extrapolated by class counts: " + "; ".join(parts)
+            sample = f"one gate per class on a 2^{n} state, extrapolated by class counts: " + "; ".join(
+                f"{counts[k]}x[{k[0]}t,{k[1]}c] {per[k]:.3f}s" for k in sorted(per))
     finally:
         if threads:
             oracle.set_num_threads(os.cpu_count() or 1)
     return value, sample, cores, extra, time.perf_counter() - t_all
+
+
+def class_counts(gates):
+    counts = {}
+    for g in gates:
+        key = (len(g.targets), len(g.controls))
+        counts[key] = counts.get(key, 0) + 1
+    return counts
+
+
+def oracle_class_times(psi, out, n, gates):
+    """Seconds the oracle takes for one gate of each (targets, controls)
+    class present in `gates` on the 2^n state psi (out = second buffer)."""
+    import oracle
+    first = {}
+    for g in gates:
+        first.setdefault((len(g.targets), len(g.controls)), g)
+    per = {}
+    for key, g in sorted(first.items()):
+        t0 = time.perf_counter()
+        oracle.apply_matrix(psi, out, n, g.targets, g.controls, g.matrix())
+        per[key] = time.perf_counter() - t0
+    return per
 
 
 def cpu_baseline_of(wl):
@@ -247,6 +262,8 @@ def run_reference(args, rank, world):
     step actually took, so ms_per_step x steps is this run's oracle time."""
     if rank != 0:
         return 0
+    if world > 1 or args.sharded_n:
+        return run_reference_sharded(args, world)
     wl = make_workload(args.workload)
     vals, walls = [], []
     for i in range(args.warmup + args.steps):
@@ -266,6 +283,47 @@ def run_reference(args, rank, world):
                          "extrapolated": extra},
         "e2e": {"value": value, "unit": "s/circuit", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_reference_sharded(args, world):
+    """Reference arm for the N > 1 headline (one QFT(34 / 35) circuit): the
+    oracle cannot hold 2^35 complex128 amplitudes (512 GiB, two buffers) in
+    host memory, so each step times one gate per (targets, controls) class of
+    that circuit on a 2^30 state and scales by 2^(n - 30) -- the oracle's cost
+    per gate is linear in the state size (labelled extrapolated)."""
+    import numpy as np
+    import oracle
+    from workloads import circuits as C
+    n = args.sharded_n or sharded_n(world)
+    big = C.qft(n)
+    counts = class_counts(big.gates)
+    small = [g for g in C.qft(30).gates]  # same gate classes, on qubits a 2^30 state has
+    cores = oracle.num_threads()
+    vals, walls = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        psi = oracle.basis_state(30, SEED_X)
+        out = np.empty_like(psi)
+        per = oracle_class_times(psi, out, 30, small)
+        del psi, out
+        v = sum(per[k] * c for k, c in counts.items()) * 2.0 ** (n - 30)
+        walls.append(time.perf_counter() - t0)
+        if i >= args.warmup:
+            vals.append(v)
+    walls = walls[args.warmup:]
+    sample = "; ".join(f"{counts[k]}x[{k[0]}t,{k[1]}c] {per[k]:.3f}s" for k in sorted(per))
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s/circuit", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
+            "higher_is_better": False, "scaling": "strong" if world >= 4 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "extrapolated": True,
+            "config": sharded_config(n, world),
+            "cpu_baseline": {"value": value, "unit": "s/circuit", "cores": cores, "kind": "oracle", "extrapolated": True,
+                             "sample": f"one gate per class on a 2^30 state, scaled by class counts of QFT{n} and "
+                                       f"2^{n - 30} (oracle cost linear in the state size): {sample}"},
+            "e2e": {"value": value, "unit": "s/circuit", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -409,6 +467,23 @@ def sharded_n(world):
     return 35 if world >= 4 else 34 if world == 2 else 30 + g
 
 
+def sharded_basis(n):
+    x = SEED_X | (0b10110 << 30) if n > 30 else SEED_X
+    return x & ((1 << n) - 1)
+
+
+def sharded_config(n, world):
+    """The config dict of the N > 1 headline (both arms)."""
+    from workloads import circuits as C
+    g = world.bit_length() - 1
+    nl = n - g
+    return {"workload": f"qft{n}_c128_sharded", "n": n, "state": "c128", "gates": len(C.qft(n)),
+            "basis": sharded_basis(n), "fuse": True, "global_qubits": g, "shard_gib": (16 << nl) / 2**30,
+            "step": "qj_state_reset + qj_apply_circuit(QJ_FUSE) + 10-qubit marginal (NCCL all-reduce)",
+            "l2": f"shard {(16 << nl) >> 30} GiB >> 126 MB L2: no flush",
+            "parallelism": f"state sharded over {world} ranks on the top {g} qubits (NCCL exchanges)"}
+
+
 def run_sharded(args, rank, world):
     """N>1 headline: one QFT(n) complex128
     circuit sharded over the N ranks on its top log2 N qubits; fused window
@@ -434,18 +509,12 @@ def run_sharded(args, rank, world):
     g = world.bit_length() - 1
     n = args.sharded_n or sharded_n(world)
     nl = n - g
-    x = SEED_X | (0b10110 << 30) if n > 30 else SEED_X
-    x &= (1 << n) - 1
+    x = sharded_basis(n)
     peak, peak_src = load_peaks()
     steps = args.steps
     line = {"metric": METRIC, "unit": "s/circuit", "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "higher_is_better": False, "scaling": "strong" if world >= 4 else "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"qft{n}_c128_sharded", "n": n, "state": "c128", "gates": len(C.qft(n)),
-                       "basis": x, "fuse": True, "global_qubits": g, "shard_gib": (16 << nl) / 2**30,
-                       "step": "qj_state_reset + qj_apply_circuit(QJ_FUSE) + 10-qubit marginal (NCCL all-reduce)",
-                       "l2": f"shard {(16 << nl) >> 30} GiB >> 126 MB L2: no flush",
-                       "parallelism": f"state sharded over {world} ranks on the top {g} qubits (NCCL exchanges)"}}
+            "dtype": "f64", "data": "synthetic", "config": sharded_config(n, world)}
 
     def emit_error(msg):
         if rank == 0:
