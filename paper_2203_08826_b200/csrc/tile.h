@@ -71,6 +71,11 @@ struct TileSpec {
     double* bins = nullptr;
     int w = 0;
     int wpos[TILE_W] = {};
+    // store in the last segment's own layout (no store transpose): window bit b
+    // is written to window position operm[b]; the planner relabels the qubit
+    // map accordingly (like an uncontrolled SWAP, R21).  identity when !operm_on
+    bool operm_on = false;
+    int8_t operm[TILE_W] = {};
     std::vector<TSeg> segs;
     std::vector<HOp> ops;        // ops in order; segs[].op0/op1 index into it
 };

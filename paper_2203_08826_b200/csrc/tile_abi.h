@@ -146,6 +146,11 @@ struct TileArgs {
     int nbq, fflags;         // fflags: 1 = synthesise the first load, 2 = fused marginal
     int8_t bin_pos[16];      // physical bit of output bit k (k = 0 is the MSB)
     uint16_t regbin[TILE_NREG];  // bin bits contributed by the last segment's register index
+    // output permutation (TileSpec::operm): the last segment stores window bit b
+    // at physical wpos[operm[b]]; tph_out = its thread-nibble offsets
+    int has_operm;
+    int8_t operm[TILE_W];
+    uint64_t tph_out[TILE_TCH][16];
     // checked JIT kernels (QJ_JIT_CHECK=1; compute-sanitizer is not available on
     // this pool): every global access is bounds-checked against namps and a
     // violation sets *chk instead of touching memory (qj_sync reports it)

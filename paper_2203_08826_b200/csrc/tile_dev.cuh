@@ -427,6 +427,14 @@ __device__ __forceinline__ uint64_t thread_phys(const TileArgs<R>& a, int s, int
     for (int c = 0; c < TILE_TCH; ++c) x |= a.tph[s][c][(tid >> (4 * c)) & 15];
     return x;
 }
+// ... of the last segment's stores (output permutation applied)
+template <typename R>
+__device__ __forceinline__ uint64_t thread_phys_out(const TileArgs<R>& a, int tid) {
+    uint64_t x = 0;
+#pragma unroll
+    for (int c = 0; c < TILE_TCH; ++c) x |= a.tph_out[c][(tid >> (4 * c)) & 15];
+    return x;
+}
 template <typename R>
 __device__ __forceinline__ uint32_t thread_loc(const TileArgs<R>& a, int s, int tid) {
     uint32_t x = 0;
@@ -520,10 +528,10 @@ template <typename R>
 __device__ __forceinline__ void tile_store(const TileArgs<R>& a, int s, const Cx<R> (&v)[TILE_NREG], uint64_t tb,
                                            int tid) {
     const TSeg& S = a.seg[s];
-    const uint64_t base = tb | thread_phys(a, s, tid);
+    const uint64_t base = tb | thread_phys_out(a, tid);  // (the last segment: s == nseg - 1)
     uint64_t rm[TILE_R];
 #pragma unroll
-    for (int j = 0; j < TILE_R; ++j) rm[j] = 1ull << a.wpos[S.rbits[j]];
+    for (int j = 0; j < TILE_R; ++j) rm[j] = 1ull << a.wpos[a.operm[S.rbits[j]]];
 #pragma unroll
     for (int r = 0; r < TILE_NREG; ++r) {
         uint64_t x = base;

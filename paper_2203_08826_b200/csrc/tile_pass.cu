@@ -85,12 +85,29 @@ bool lower_tile(const TileSpec& t, int nl, TileArgs<R>* a, std::vector<unsigned 
     a->nbq = t.nbins_q;
     a->fflags = (t.synth ? 1 : 0) | (t.nbins_q > 0 ? 2 : 0);
     for (int k = 0; k < t.nbins_q; ++k) a->bin_pos[k] = t.bin_pos[k];
-    if (t.nbins_q > 0) {  // register-index part of the bin for the last segment's mapping
+    // output positions of window bits (identity unless the last segment stores in its own layout)
+    a->has_operm = t.operm_on ? 1 : 0;
+    int opos[TILE_W];
+    for (int b = 0; b < TILE_W; ++b) {
+        a->operm[b] = (int8_t)(t.operm_on ? t.operm[b] : b);
+        opos[b] = t.wpos[a->operm[b]];
+    }
+    {
+        const TSeg& S = t.segs.back();
+        for (int half = 0; half < TILE_TCH; ++half)
+            for (int nib = 0; nib < 16; ++nib) {
+                uint64_t ph = 0;
+                for (int q = 0; q < 4; ++q)
+                    if (((nib >> q) & 1) && half * 4 + q < TILE_T) ph |= 1ull << opos[S.tbits[half * 4 + q]];
+                a->tph_out[half][nib] = ph;
+            }
+    }
+    if (t.nbins_q > 0) {  // register-index part of the bin for the last segment's (output) mapping
         const TSeg& S = t.segs.back();
         for (int r = 0; r < TILE_NREG; ++r) {
             uint64_t x = 0;
             for (int j = 0; j < TILE_R; ++j)
-                if ((r >> j) & 1) x |= 1ull << t.wpos[S.rbits[j]];
+                if ((r >> j) & 1) x |= 1ull << opos[S.rbits[j]];
             uint32_t b = 0;
             for (int k = 0; k < t.nbins_q; ++k) b = (b << 1) | (uint32_t)((x >> t.bin_pos[k]) & 1u);
             a->regbin[r] = (uint16_t)b;

@@ -261,11 +261,17 @@ static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, 
     flush(0, true);
     // the first and last segments touch HBM: their register bits must avoid the low bits
     if (segs.front().rsel & lowsel) segs.insert(segs.begin(), SegB());
-    if (segs.back().rsel & lowsel) segs.emplace_back();
+    // a last segment whose registers hold low window bits stores in its own
+    // layout: its lanes' window bits are written to the low physical bits
+    // (coalesced) and the window bits are relabelled (TileSpec::operm, the
+    // planner updates the qubit map) instead of one more SMEM transpose
+    static const bool operm_ok = !(getenv("QJ_TILE_OPERM") && getenv("QJ_TILE_OPERM")[0] == '0');
+    const bool operm = operm_ok && segs.size() > 1 && (segs.back().rsel & lowsel);
+    if ((segs.back().rsel & lowsel) && !operm) segs.emplace_back();
     if ((int)segs.size() > TILE_MAXSEG) return false;
     // pad register sets to TILE_R bits (prefer high window bits)
     for (size_t s = 0; s < segs.size(); ++s) {
-        const bool global = (s == 0 || s + 1 == segs.size());
+        const bool global = s == 0 || (s + 1 == segs.size() && !operm);
         for (int j = TILE_W - 1; j >= 0 && popc(segs[s].rsel) < TILE_R; --j) {
             if (global && ((lowsel >> j) & 1)) continue;
             segs[s].rsel |= 1u << j;
@@ -274,7 +280,7 @@ static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, 
     for (size_t s = 0; s < segs.size(); ++s) {
         TSeg S;
         std::memset(&S, 0, sizeof(S));
-        const bool global = (s == 0 || s + 1 == segs.size());
+        const bool global = s == 0 || (s + 1 == segs.size() && !operm);
         for (int j = 0, k = 0; j < TILE_W; ++j)
             if ((segs[s].rsel >> j) & 1) S.rbits[k++] = (int8_t)j;
         thread_bits(segs[s].rsel, C, M, global, S.tbits);
@@ -283,6 +289,17 @@ static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, 
         S.op1 = (uint16_t)ts.ops.size();
         S.split = -1;
         ts.segs.push_back(S);
+    }
+    if (operm) {  // lanes 0..C-1 of the last segment -> window positions 0..C-1, the rest in order
+        const TSeg& L = ts.segs.back();
+        bool used[TILE_W] = {};
+        for (int i = 0; i < C; ++i) {
+            ts.operm[L.tbits[i]] = (int8_t)i;
+            used[L.tbits[i]] = true;
+        }
+        for (int b = 0, pos = C; b < TILE_W; ++b)
+            if (!used[b]) ts.operm[b] = (int8_t)pos++;
+        ts.operm_on = true;
     }
     // Half-buffer transposes: the move into segment s can run
     // in two rounds through a buffer of 2^(W-1) amplitudes when one window bit
@@ -390,6 +407,13 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
                     sr.shard = r;
                     sr.tile.gbase = (uint64_t)r << ctx.nl;
                     out.push_back(std::move(sr));
+                }
+                if (s.tile.operm_on) {  // the pass wrote window bit b at window position operm[b]
+                    int where[64];
+                    for (int b = 0; b < 64; ++b) where[b] = b;
+                    for (int b = 0; b < TILE_W; ++b) where[s.tile.wpos[b]] = s.tile.wpos[s.tile.operm[b]];
+                    for (int& p : phys)
+                        if (p < 64) p = where[p];
                 }
             } else {
                 // cannot happen with the limits below; stay correct anyway
