@@ -176,7 +176,8 @@ void thread_bits(uint32_t rsel, int C, int M, bool global, int8_t* tb) {
 // end of the pass and touch a bit outside the window are left out of the pass
 // and returned, so the caller can move them to the front of the next pass
 // (they commute with everything in between).
-static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, std::vector<int>* carried = nullptr) {
+static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, std::vector<int>* carried = nullptr,
+                       bool final_pass = false) {
     // window: pad to TILE_W bits with the highest unused local bits
     uint64_t W = pb.W;
     for (int b = nl - 1; b >= 0 && popc(W) < TILE_W; --b) W |= 1ull << b;
@@ -265,8 +266,13 @@ static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, 
     // layout: its lanes' window bits are written to the low physical bits
     // (coalesced) and the window bits are relabelled (TileSpec::operm, the
     // planner updates the qubit map) instead of one more SMEM transpose
-    static const bool operm_ok = !(getenv("QJ_TILE_OPERM") && getenv("QJ_TILE_OPERM")[0] == '0');
-    const bool operm = operm_ok && segs.size() > 1 && (segs.back().rsel & lowsel);
+    // Only the plan's final pass: a relabelled window changes which qubits sit
+    // on the low bits for the passes after it (measured: QAOA30's later passes
+    // lost more than the saved transposes, 44.0 -> 52.7 ms; QFT30's final pass
+    // 6.22 -> 5.79 ms).  QJ_TILE_OPERM=0 off, =2 on every pass.
+    static const char* operm_env = getenv("QJ_TILE_OPERM");
+    const int operm_mode = operm_env ? atoi(operm_env) : 1;
+    const bool operm = operm_mode > 0 && (final_pass || operm_mode == 2) && segs.size() > 1 && (segs.back().rsel & lowsel);
     if ((segs.back().rsel & lowsel) && !operm) segs.emplace_back();
     if ((int)segs.size() > TILE_MAXSEG) return false;
     // pad register sets to TILE_R bits (prefer high window bits)
@@ -371,7 +377,7 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
             // opt-in (QJ_TILE_CARRY=1): measured slower -- the next pass's anchored runs
             // gain per-tile factors
             const bool carry = allow_carry && has_op && getenv("QJ_TILE_CARRY") && getenv("QJ_TILE_CARRY")[0] == '1';
-            if (build_tile(pb, ctx.nl, C, M, s.tile, carry ? &carried : nullptr) &&
+            if (build_tile(pb, ctx.nl, C, M, s.tile, carry ? &carried : nullptr, !allow_carry) &&
                 tile_fits(s.tile, ctx.nl, ctx.amp_bytes)) {
                 for (int i : carried) {
                     next.nterms += (int)pb.items[i].terms.size();
