@@ -398,6 +398,13 @@ qj_status qj_plan_canonicalize(int n, int nshards, const int* phys_in, qj_plan_s
 qj_status qj_debug_tile_sources(int n, int amp_bytes, const qj_gate* gates, int ngates, uint32_t flags,
                                 const char* dir, int compile, int* nkernels);
 
+/* Tooling: run the NCCL exchange machinery (pipelined grouped send / recv
+ * through the staging ring, pack / unpack kernels, two streams) with this
+ * rank as its own partner on the half of its shard whose `local_bit` is 1.
+ * The state must come back unchanged; used to exercise the multi-GPU data
+ * path on one GPU.  Errors: INVALID_ARG (not an NCCL state), INDEX, NCCL, CUDA. */
+qj_status qj_debug_nccl_self_exchange(qj_state s, int local_bit);
+
 /* The paper's gate fusion (Table 2 Gates* / Depth*), host
  * only: greedily combine the circuit into gates of at most `max_qubits` (1 to
  * 5; the paper's fusion is 2) qubits.  Fused groups come back as

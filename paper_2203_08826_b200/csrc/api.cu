@@ -291,11 +291,15 @@ int prof_kind(const Step& st) {
 // Exchange over NCCL (dist.h): this rank trades the half of its shard whose
 // local bit L equals spec.half_bit with the partner, chunk by chunk through
 // the staging ring.
-qj_status nccl_exchange(qj_state s, int j, int L) {
+qj_status nccl_exchange_with(qj_state s, const ExchangeSpec& ex, int L);
+
+qj_status nccl_exchange(qj_state s, int j, int L) { return nccl_exchange_with(s, exchange_spec(s->rank, j), L); }
+
+// The exchange proper (also driven directly by qj_debug_nccl_self_exchange).
+qj_status nccl_exchange_with(qj_state s, const ExchangeSpec& ex, int L) {
     const char* why = nullptr;
     const NcclApi* api = nccl_api(&why);
     if (!api) return fail(QJ_ERR_NCCL, "NCCL unavailable: %s", why ? why : "?");
-    const ExchangeSpec ex = exchange_spec(s->rank, j);
     const uint64_t half = 1ull << (s->nl - 1);
     const uint64_t chunk = std::min<uint64_t>(half, (uint64_t)(256ull << 20) / (uint64_t)s->amp_bytes);
     const bool contiguous = (L == s->nl - 1);
@@ -1980,6 +1984,15 @@ qj_status qj_debug_tile_sources(int n, int amp_bytes, const qj_gate* gates, int 
     }
     *nkernels = k;
     return QJ_OK;
+}
+
+qj_status qj_debug_nccl_self_exchange(qj_state s, int local_bit) {
+    if (!s || !s->comm) return fail(QJ_ERR_INVALID_ARG, "needs an NCCL-backed state");
+    if (local_bit < 0 || local_bit >= s->nl) return fail(QJ_ERR_INDEX_OUT_OF_RANGE, "local bit %d", local_bit);
+    ExchangeSpec ex;
+    ex.peer = s->rank;  // this rank trades the half with itself: the state must come back unchanged
+    ex.half_bit = 1;
+    return nccl_exchange_with(s, ex, local_bit);
 }
 
 qj_status qj_sync(qj_state s) {

@@ -116,6 +116,9 @@ __device__ __forceinline__ uint64_t group_base(uint64_t g, const TcArgs& a) {
     return x | a.fix_val;
 }
 
+constexpr int kStageStride = 33;  // float2 per staged row (32 members + 1 pad: 2-way bank conflicts at most)
+
+template <bool STAGED>
 __global__ void __launch_bounds__(kTcThreads, 1) dense5_tc_kernel(const __grid_constant__ TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     unsigned char* yhi = smraw;
@@ -163,13 +166,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense5_tc_kernel(const __grid_c
     uint64_t t = (uint64_t)blockIdx.x * kTcWorkers + wk;
     const uint64_t tstep = (uint64_t)gridDim.x * kTcWorkers;
     uint64_t base = 0;
-    if (t < ntiles) {
-        base = group_base(t * kTcRows + row, a);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __ldcs(psi + base + a.moff[j]);
+    // staged form: this thread's share of every tile is L = row + 128 m
+    float2* stage = reinterpret_cast<float2*>(xhi);  // aliases X hi / lo (free between MMAs)
+    uint64_t arow = 0;
+    uint32_t srow = 0;
+    if constexpr (STAGED) {
+        for (int i = 0; i < 7; ++i)
+            if ((row >> i) & 1) {
+                arow |= 1ull << a.lpos_row[i];
+                srow += a.w_row[i];
+            }
     }
+    auto load_tile = [&](uint64_t tt) {
+        if constexpr (STAGED) {
+            const uint64_t tb = group_base(tt * kTcRows, a) | arow;
+#pragma unroll 8
+            for (int m = 0; m < 32; ++m) stage[srow + a.sidx_m[m]] = __ldcs(psi + (tb | a.addr_m[m]));
+            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = stage[row * kStageStride + j];
+            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");  // staging free for X
+        } else {
+            base = group_base(tt * kTcRows + row, a);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __ldcs(psi + base + a.moff[j]);
+        }
+    };
+    if (!STAGED && t < ntiles) load_tile(t);
     uint32_t phase = 0;
     for (; t < ntiles; t += tstep, phase ^= 1) {
+        if constexpr (STAGED) load_tile(t);
         // X hi / lo of this thread's group (row): K = (Re v_0..31, Im v_0..31)
 #pragma unroll
         for (int c = 0; c < 16; ++c) {  // 4 consecutive k per 16-byte store
@@ -206,17 +232,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense5_tc_kernel(const __grid_c
         // prefetch the next tile's amplitudes while the MMAs run
         const uint64_t cur = base;
         const uint64_t tn = t + tstep;
-        if (tn < ntiles) {
-            base = group_base(tn * kTcRows + row, a);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __ldcs(psi + base + a.moff[j]);
-        }
+        if (!STAGED && tn < ntiles) load_tile(tn);
         mbar_wait_parity(&bars[wk], phase);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         float o[64];
         tmem_ld64(tload, o);
+        if constexpr (STAGED) {  // rows -> staging -> cooperative coalesced stores
 #pragma unroll
-        for (int j = 0; j < 32; ++j) __stcs(psi + cur + a.moff[j], make_float2(o[j], o[32 + j]));
+            for (int j = 0; j < 32; ++j) stage[row * kStageStride + j] = make_float2(o[j], o[32 + j]);
+            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");
+            const uint64_t tb = group_base(t * kTcRows, a) | arow;
+#pragma unroll 8
+            for (int m = 0; m < 32; ++m) __stcs(psi + (tb | a.addr_m[m]), stage[srow + a.sidx_m[m]]);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // staging (X) is rewritten next tile
+            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) __stcs(psi + cur + a.moff[j], make_float2(o[j], o[32 + j]));
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -266,15 +299,58 @@ cudaError_t run_dense_tc(const Pass& p, void* psi, int nl, cudaStream_t st, Laun
     a->nins = np;
     for (int i = 0; i < np; ++i) a->ins_pos[i] = pos[i];
     a->ngroups = 1ull << (nl - np);
+    // staged when a thread's own 32 members would not be coalesced across a warp
+    // (some target or fixed bit below bit 5: the warp's groups are not 32
+    // consecutive amplitudes)
+    a->staged = pos[0] < 5 ? 1 : 0;
+    if (a->staged) {
+        int lpos[12], ltype[12], nlp = 0, k = 0;  // ltype: 0..6 group bit k, 100 + t target t
+        for (int b = 0; nlp < 12 && b < nl; ++b) {
+            bool ins = false;
+            for (int i = 0; i < np; ++i) ins |= pos[i] == b;
+            int tt = -1;
+            for (int i = 0; i < 5; ++i)
+                if (p.tpos[i] == b) tt = i;
+            if (tt >= 0) {
+                lpos[nlp] = b;
+                ltype[nlp++] = 100 + tt;
+            } else if (!ins && k < 7) {
+                lpos[nlp] = b;
+                ltype[nlp++] = k++;
+            }
+        }
+        if (nlp != 12) return cudaErrorInvalidValue;
+        auto weight = [&](int i) -> uint32_t {
+            return ltype[i] >= 100 ? (1u << (4 - (ltype[i] - 100))) : (uint32_t)kStageStride << ltype[i];
+        };
+        for (int i = 0; i < 7; ++i) {
+            a->lpos_row[i] = lpos[i];
+            a->w_row[i] = weight(i);
+        }
+        for (int m = 0; m < 32; ++m) {
+            uint64_t ad = 0;
+            uint32_t sx = 0;
+            for (int i = 0; i < 5; ++i)
+                if ((m >> i) & 1) {
+                    ad |= 1ull << lpos[7 + i];
+                    sx += weight(7 + i);
+                }
+            a->addr_m[m] = ad;
+            a->sidx_m[m] = sx;
+        }
+    }
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dense5_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+        cudaError_t e = cudaFuncSetAttribute(dense5_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dense5_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const uint64_t ntiles = a->ngroups / kTcRows;
     const uint64_t grid = std::min<uint64_t>((ntiles + kTcWorkers - 1) / kTcWorkers, (uint64_t)device_sms());
-    dense5_tc_kernel<<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(*a);
+    if (a->staged) dense5_tc_kernel<true><<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(*a);
+    else dense5_tc_kernel<false><<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(*a);
     ls.launches++;
     return cudaGetLastError();
 }

@@ -20,6 +20,15 @@ struct TcArgs {
     uint64_t fix_val;     // fixed bits (controls = 1)
     uint64_t ngroups;     // 2^(nl - nins)
     void* psi;
+    // staged form (a target or fixed bit below bit 5: a thread's own members
+    // would be uncoalesced): a tile's 4096 amplitudes, indexed by L whose 12
+    // bits are the 7 lowest free positions and the 5 target positions in
+    // ascending physical order, move through shared memory cooperatively
+    int staged;
+    int lpos_row[7];      // physical position of L bits 0..6 (a thread's row index)
+    uint32_t w_row[7];    // staging index weight of L bits 0..6
+    uint64_t addr_m[32];  // physical offset of L bits 7..11 (m = L >> 7)
+    uint32_t sidx_m[32];  // staging index of L bits 7..11
 };
 
 // QJ_TC=0 keeps every dense pass on the CUDA cores.

@@ -37,7 +37,8 @@ EXPORTS = ["qj_state_init", "qj_state_init_sharded", "qj_state_reset", "qj_state
            "qj_insert_zero_bits", "qj_set_profiling", "qj_get_profile", "qj_state_canonicalize",
            "qj_plan_circuit", "qj_exchange_peer", "qj_fuse_circuit", "qj_collapse",
            "qj_sample_distribution", "qj_sample", "qj_measure", "qj_state_init_host",
-           "qj_simulate", "qj_state_layout", "qj_plan_canonicalize", "qj_debug_tile_sources"]
+           "qj_simulate", "qj_state_layout", "qj_plan_canonicalize", "qj_debug_tile_sources",
+           "qj_debug_nccl_self_exchange"]
 
 
 class QJError(RuntimeError):
@@ -123,6 +124,7 @@ def lib():
         "qj_exchange_peer": ([I, I, IP, IP], None),
         "qj_plan_canonicalize": ([I, I, IP, ctypes.POINTER(qj_plan_step), I, IP], S),
         "qj_debug_tile_sources": ([I, I, ctypes.POINTER(qj_gate), I, ctypes.c_uint32, ctypes.c_char_p, I, IP], S),
+        "qj_debug_nccl_self_exchange": ([P, I], S),
         "qj_fuse_circuit": ([I, ctypes.POINTER(qj_gate), I, I, ctypes.POINTER(qj_gate), ctypes.POINTER(ctypes.c_double),
                              I, IP, IP], S),
         "qj_collapse": ([P, IP, I, U64, ctypes.POINTER(ctypes.c_double)], S),
@@ -595,6 +597,11 @@ class State:
         _check(lib().qj_get_profile(self._h, arr, 16, ctypes.byref(cnt), 1 if reset else 0))
         return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
                                        "alg_bytes": arr[i].alg_bytes} for i in range(cnt.value)}
+
+    def debug_self_exchange(self, local_bit):
+        """NCCL states only: the exchange path with this rank as its own partner
+        (the state must come back unchanged)."""
+        _check(lib().qj_debug_nccl_self_exchange(self._h, int(local_bit)))
 
     def layout(self):
         """Logical->physical bit map: qubit q is held at bit layout()[q]."""

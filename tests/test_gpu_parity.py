@@ -334,9 +334,21 @@ def _nccl_worker(port, q):
         full = st.probabilities().cpu().numpy()
         st.sync()
         exp = oracle.run(circ, oracle.basis_state(n, 5))
+        # the exchange data path (pipelined grouped send / recv through the
+        # staging ring, both streams, pack / unpack) with this rank as its own
+        # partner: a 1 GiB shard (two 256 MiB chunks per half), the top local
+        # bit (in-place halves) and a low bit (pack / unpack); unchanged after
+        n2 = 26
+        t2 = torch.randn(2**n2, dtype=torch.complex128, device="cuda")
+        ref = t2.clone()
+        s2 = qjp.State.distributed(t2, n2, basis=None)
+        for bit in (n2 - 1, 3, 0):
+            s2.debug_self_exchange(bit)
+        s2.sync()
+        self_ok = bool(torch.equal(t2, ref))
         q.put((float(np.max(np.abs(t.cpu().numpy() - exp))),
                float(np.max(np.abs(p - oracle.probabilities(exp, n, [0, 3, 7])))),
-               float(np.max(np.abs(full - np.abs(exp) ** 2))), st.info()["nshards"]))
+               float(np.max(np.abs(full - np.abs(exp) ** 2))), st.info()["nshards"], self_ok))
     finally:
         dist.destroy_process_group()
 
@@ -354,8 +366,9 @@ def test_nccl_single_rank_state():
     p.start()
     p.join(timeout=300)
     assert p.exitcode == 0
-    e_amp, e_marg, e_full, nsh = q.get(timeout=10)
+    e_amp, e_marg, e_full, nsh, self_ok = q.get(timeout=10)
     assert nsh == 1 and e_amp < 1e-12 and e_marg < 1e-12 and e_full < 1e-12
+    assert self_ok, "self exchange changed the state"
 
 
 # ------------------------------------------------ edge cases
