@@ -178,9 +178,15 @@ void thread_bits(uint32_t rsel, int C, int M, bool global, int8_t* tb) {
 // (they commute with everything in between).
 static bool build_tile(const PassBuild& pb, int nl, int C, int M, TileSpec& ts, std::vector<int>* carried = nullptr,
                        bool final_pass = false) {
-    // window: pad to TILE_W bits with the highest unused local bits
+    // window: pad to TILE_W bits with unused local bits -- the lowest ones
+    // (QJ_TILE_PAD=low: longer contiguous HBM rows) or the highest (default)
     uint64_t W = pb.W;
-    for (int b = nl - 1; b >= 0 && popc(W) < TILE_W; --b) W |= 1ull << b;
+    static const bool pad_low = getenv("QJ_TILE_PAD") && getenv("QJ_TILE_PAD")[0] == 'l';
+    if (pad_low) {
+        for (int b = 0; b < nl && popc(W) < TILE_W; ++b) W |= 1ull << b;
+    } else {
+        for (int b = nl - 1; b >= 0 && popc(W) < TILE_W; --b) W |= 1ull << b;
+    }
     if (popc(W) != TILE_W) return false;
     ts = TileSpec();
     ts.w = TILE_W;
