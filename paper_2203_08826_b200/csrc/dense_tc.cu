@@ -177,25 +177,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense5_tc_kernel(const __grid_c
                 srow += a.w_row[i];
             }
     }
+    // (staged form: the next tile's amplitudes are loaded coalesced into v in
+    // L order while the MMAs run, and redistributed to rows through shared
+    // memory at the start of the tile)
     auto load_tile = [&](uint64_t tt) {
         if constexpr (STAGED) {
             const uint64_t tb = group_base(tt * kTcRows, a) | arow;
-#pragma unroll 8
-            for (int m = 0; m < 32; ++m) stage[srow + a.sidx_m[m]] = __ldcs(psi + (tb | a.addr_m[m]));
-            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = stage[row * kStageStride + j];
-            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");  // staging free for X
+            for (int m = 0; m < 32; ++m) v[m] = __ldcs(psi + (tb | a.addr_m[m]));
         } else {
             base = group_base(tt * kTcRows + row, a);
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __ldcs(psi + base + a.moff[j]);
         }
     };
-    if (!STAGED && t < ntiles) load_tile(t);
+    if (t < ntiles) load_tile(t);
     uint32_t phase = 0;
     for (; t < ntiles; t += tstep, phase ^= 1) {
-        if constexpr (STAGED) load_tile(t);
+        if constexpr (STAGED) {  // L order -> rows
+#pragma unroll
+            for (int m = 0; m < 32; ++m) stage[srow + a.sidx_m[m]] = v[m];
+            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = stage[row * kStageStride + j];
+            asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wk), "r"(kTcRows) : "memory");  // staging free for X
+        }
         // X hi / lo of this thread's group (row): K = (Re v_0..31, Im v_0..31)
 #pragma unroll
         for (int c = 0; c < 16; ++c) {  // 4 consecutive k per 16-byte store
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) dense5_tc_kernel(const __grid_c
         // prefetch the next tile's amplitudes while the MMAs run
         const uint64_t cur = base;
         const uint64_t tn = t + tstep;
-        if (!STAGED && tn < ntiles) load_tile(tn);
+        if (tn < ntiles) load_tile(tn);
         mbar_wait_parity(&bars[wk], phase);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         float o[64];

@@ -415,3 +415,35 @@ def test_checked_tile_kernels_subprocess():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "sanitize driver done" in r.stdout
+
+
+# ------------------------------------------------ BV30: every amplitude against its closed form
+@pytest.mark.slow
+def test_bv30_simulate_every_amplitude():
+    """Bernstein-Vazirani (Table 2 row bv, secret all ones,
+    ancilla = qubit 29): the output is |1...1>_data (x) |->_anc, i.e. +1/sqrt2 at
+    canonical index 2^30 - 2, -1/sqrt2 at 2^30 - 1 and exactly 0 elsewhere.  The
+    bench step (qj_simulate, fused marginal over qubits 0..9 = all ones with
+    probability 1); all 2^30 amplitudes checked after canonicalisation."""
+    n = 30
+    t = torch.empty(2**n, dtype=torch.complex128, device="cuda")
+    st = qjp.State(t, basis=None)
+    t.fill_(float("nan"))
+    p = st.simulate(0, C.bv(n).gates, qubits=list(range(10)))
+    st.canonicalize()
+    st.sync()
+    pc = p.cpu().numpy()
+    assert abs(pc[1023] - 1.0) <= 1e-12 and np.max(np.abs(pc[:1023])) <= 1e-12
+    chunk = CHUNK
+    host = torch.empty(chunk, dtype=t.dtype, pin_memory=True)
+    worst = 0.0
+    for off in range(0, 2**n, chunk):
+        host.copy_(t[off:off + chunk])
+        a = host.numpy().copy()
+        if off + chunk == 2**n:
+            assert abs(a[-2] - 2**-0.5) <= 1e-12 and abs(a[-1] + 2**-0.5) <= 1e-12
+            a[-2:] = 0
+        worst = max(worst, float(np.max(np.abs(a))))
+    assert worst <= 1e-12, f"max |amp| off the two basis states {worst:.3e}"
+    del st, t
+    torch.cuda.empty_cache()

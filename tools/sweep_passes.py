@@ -35,7 +35,12 @@ def emit(d):
     print(json.dumps(d), flush=True)
 
 
+FILTER = os.environ.get("SWEEP_FILTER")  # only entries whose label contains it
+
+
 def timed_gates(st, gates, fuse, label, dt):
+    if FILTER and FILTER not in label:
+        return
     packed = st.pack_circuit(gates)
     st.apply_circuit(None, fuse=fuse, packed=packed)  # plan + JIT
     st.sync()
