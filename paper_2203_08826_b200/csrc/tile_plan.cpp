@@ -454,7 +454,11 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
     std::vector<int> remaining(gates.size());
     for (size_t i = 0; i < gates.size(); ++i) remaining[i] = (int)i;
     std::vector<char> blocked(ctx.n, 0);
-    double budget = ctx.amp_bytes == 16 ? 96.0 : 96.0;
+    // arithmetic per amplitude a pass may take before it closes (cost units of
+    // op_cost); swept on B200 with the zero-pattern cost model (round 2:
+    // sup32 c64 915 -> 800 / 762 ms at 128 / 192, QAOA30 c128 44.9 -> 42.5 ms at
+    // 128 but 46.7 at 192, var20 / tfim20 best at 128-192)
+    double budget = ctx.amp_bytes == 16 ? 128.0 : 192.0;
     if (const char* b = getenv("QJ_TILE_BUDGET")) budget = atof(b);
     const bool dag = !(getenv("QJ_TILE_DAG") && getenv("QJ_TILE_DAG")[0] == '0');
     while (!remaining.empty()) {
