@@ -455,10 +455,11 @@ void Planner::plan_fused(const PlanContext& ctx, const std::vector<LGate>& gates
     for (size_t i = 0; i < gates.size(); ++i) remaining[i] = (int)i;
     std::vector<char> blocked(ctx.n, 0);
     // arithmetic per amplitude a pass may take before it closes (cost units of
-    // op_cost); swept on B200 with the zero-pattern cost model (round 2:
-    // sup32 c64 915 -> 800 / 762 ms at 128 / 192, QAOA30 c128 44.9 -> 42.5 ms at
-    // 128 but 46.7 at 192, var20 / tfim20 best at 128-192)
-    double budget = ctx.amp_bytes == 16 ? 128.0 : 192.0;
+    // op_cost); swept on B200 with the zero-pattern cost model (round 2): c64
+    // sup32 915 -> 800 / 762 ms at 128 / 192; c128 stays at 96 -- at 128 QAOA30
+    // gains 44.9 -> 43.0 ms but BV30's pre-fused plan wins the byte comparison
+    // with a compute-heavy pass (8.7 -> 18.4 ms)
+    double budget = ctx.amp_bytes == 16 ? 96.0 : 192.0;
     if (const char* b = getenv("QJ_TILE_BUDGET")) budget = atof(b);
     const bool dag = !(getenv("QJ_TILE_DAG") && getenv("QJ_TILE_DAG")[0] == '0');
     while (!remaining.empty()) {
