@@ -23,6 +23,7 @@ struct JitKernel {
     int blocks = 2;  // resident CTAs per SM it was compiled for (grid = SMs x blocks)
     int threads = TILE_THREADS;  // block size (ring form: two workers)
     bool tmap = false;           // ring form with TMA tensor loads: TileArgs::tmap must be encoded
+    bool l2_256 = false;         // ... with 256-byte L2 promotion (sibling-pair tile order)
 };
 
 // Checked JIT kernels (QJ_JIT_CHECK=1): the device flag their bounds checks
@@ -32,7 +33,7 @@ bool tile_check_failed();
 
 // Encode the ring form's tensor map (TileArgs::tmap) for a->psi.
 template <typename R>
-cudaError_t tile_jit_encode_tmap(TileArgs<R>* a);
+cudaError_t tile_jit_encode_tmap(TileArgs<R>* a, bool l2_256 = false);
 
 // The specialised kernel for this lowered pass (compiled and cached on first
 // use; `blob` is the host copy of the pass's program buffer), or nullptr with

@@ -549,7 +549,7 @@ cudaError_t run_tile(const TileSpec& t, void* psi, int nl, cudaStream_t st, Tile
     if (jk) {
         tile_jit_fill<R>(*jk, a, blob.data());
         if (jk->tmap) {
-            e = tile_jit_encode_tmap<R>(a);
+            e = tile_jit_encode_tmap<R>(a, jk->l2_256);
             if (e != cudaSuccess) return e;
         }
         const uint64_t jgrid = std::min<uint64_t>(a->ntiles, (uint64_t)sms * jk->blocks);
@@ -595,7 +595,7 @@ cudaError_t tile_prepare(const TileSpec& t, void* psi, int nl, PreparedTile& out
     if (jk) {
         tile_jit_fill<R>(*jk, a, blob.data());
         if (jk->tmap) {
-            cudaError_t e = tile_jit_encode_tmap<R>(a);
+            cudaError_t e = tile_jit_encode_tmap<R>(a, jk->l2_256);
             if (e != cudaSuccess) return e;
         }
         out.smem += jk->smem_extra;
