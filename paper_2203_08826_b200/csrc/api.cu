@@ -1496,9 +1496,85 @@ qj_status qj_measure(qj_state s, const int* qubits, int nq, uint64_t seed, uint6
 
 // ------------------------------------------------------------------ qj_simulate
 // QJ_LIVE_TILES=0 runs every later tile pass over the whole state (A/B check)
+// Live-tile passes: amplitudes whose newly windowed bits not yet touched by a
+// segment's register ops differ from the basis are still zero, so the JIT
+// skips their transposes and arithmetic (tile_jit.cpp, zero tracking).  Put
+// those still-constrained thread bits of every later segment on warp bits
+// (thread-id bits >= 5; lanes 0..4 keep their bank-conflict / store roles) so
+// the skips are warp-uniform.
+static void live_thread_order(TileSpec& t, int amp_bytes) {
+    const int M = amp_bytes == 16 ? 3 : 4;  // lanes 0..M-1: swizzle residues / the output's low bits
+    uint32_t zl = 0;  // window-local zero mask
+    for (int j = 0; j < TILE_W; ++j)
+        if ((t.zero_mask >> t.wpos[j]) & 1) zl |= 1u << j;
+    uint32_t cons = zl;
+    for (size_t s = 0; s < t.segs.size(); ++s) {
+        TSeg& S = t.segs[s];
+        uint32_t rsel = 0;
+        for (int j = 0; j < TILE_R; ++j) rsel |= 1u << S.rbits[j];
+        if (s > 0) {
+            // constrained thread bits to the top thread-id positions, order otherwise kept
+            std::vector<int8_t> lanes(S.tbits, S.tbits + std::min(5, TILE_T)), rest, hot;
+            for (int i = std::min(5, TILE_T); i < TILE_T; ++i)
+                ((cons >> S.tbits[i]) & 1 ? hot : rest).push_back(S.tbits[i]);
+            // a constrained lane bit moves up too when a warp position is free for it
+            for (int i = std::min(5, TILE_T) - 1; i >= M && !rest.empty(); --i)
+                if ((cons >> lanes[i]) & 1) {
+                    hot.push_back(lanes[i]);
+                    lanes[i] = rest.front();
+                    rest.erase(rest.begin());
+                }
+            int k = 0;
+            for (int8_t b : lanes) S.tbits[k++] = b;
+            for (int8_t b : rest) S.tbits[k++] = b;
+            for (int8_t b : hot) S.tbits[k++] = b;
+        }
+        cons &= ~rsel;
+    }
+}
+
 static bool live_tiles_on() {
     static const bool on = !(getenv("QJ_LIVE_TILES") && getenv("QJ_LIVE_TILES")[0] == '0');
     return on;
+}
+
+// qj_simulate from |basis>: the first tile pass synthesises the one tile
+// holding the basis amplitude; the run of tile passes after it runs only the
+// live tiles (§5.2 "Live tiles").  Returns whether no init kernel is needed.
+static bool setup_live_tiles(std::vector<Step>& steps, int nl, int amp_bytes, uint64_t basis) {
+    bool init_none = false;
+    Step& f = steps.front();
+    f.tile.synth = true;
+    f.tile.synth_index = basis;
+    f.alg_bytes = 2.0 * amp_bytes * std::ldexp(1.0, TILE_W);  // one live tile (the rest: init kernel)
+    // the run of tile passes after it: amplitudes whose bits outside
+    // every window so far differ from |basis> are still zero, and each
+    // pass maps every tile onto itself, so only the tiles whose
+    // not-yet-windowed bits equal the basis bits are live
+    const uint64_t all = nl >= 64 ? ~0ull : (1ull << nl) - 1;
+    uint64_t windowed = 0;
+    for (size_t i = 0; i < steps.size() && steps[i].type == Step::TILE && live_tiles_on(); ++i) {
+        Step& t = steps[i];
+        uint64_t wm = 0;
+        for (int j = 0; j < TILE_W; ++j) wm |= 1ull << t.tile.wpos[j];
+        if (i == 0) {  // the synthesised pass: the one tile holding x is the grid
+            t.tile.fix_mask = all & ~wm;
+            t.tile.fix_val = basis & t.tile.fix_mask;
+        } else {
+            t.tile.fix_mask = all & ~windowed & ~wm;
+            t.tile.fix_val = basis & t.tile.fix_mask;
+            t.tile.zero_mask = wm & ~windowed;
+            t.tile.zero_val = basis & t.tile.zero_mask;
+            if (!(getenv("QJ_ZSPARSE") && getenv("QJ_ZSPARSE")[0] == '0')) live_thread_order(t.tile, amp_bytes);
+            const int fb = __builtin_popcountll(t.tile.fix_mask), z = __builtin_popcountll(t.tile.zero_mask);
+            t.alg_bytes = amp_bytes * (std::ldexp(1.0, nl - fb - z) + std::ldexp(1.0, nl - fb));
+            // each pass reads only amplitudes the previous one wrote: once a
+            // pass writes every tile, no amplitude is read before it is written
+            if (!t.tile.fix_mask) init_none = true;
+        }
+        windowed |= wm;
+    }
+    return init_none;
 }
 static qj_status run_sim(qj_state s, qj_state_s::CachedPlan& p) {
     cudaError_t e = cudaSuccess;
@@ -1603,38 +1679,7 @@ qj_status qj_simulate(qj_state s, uint64_t basis, const qj_gate* gates, int ngat
         const bool first_tile = !p->steps.empty() && p->steps.front().type == Step::TILE;
         const bool last_tile = !p->steps.empty() && p->steps.back().type == Step::TILE;
         p->init_first = !first_tile;
-        if (first_tile) {
-            Step& f = p->steps.front();
-            f.tile.synth = true;
-            f.tile.synth_index = basis;
-            f.alg_bytes = 2.0 * s->amp_bytes * std::ldexp(1.0, TILE_W);  // one live tile (the rest: init kernel)
-            // the run of tile passes after it: amplitudes whose bits outside
-            // every window so far differ from |basis> are still zero, and each
-            // pass maps every tile onto itself, so only the tiles whose
-            // not-yet-windowed bits equal the basis bits are live
-            const uint64_t all = s->nl >= 64 ? ~0ull : (1ull << s->nl) - 1;
-            uint64_t windowed = 0;
-            for (size_t i = 0; i < p->steps.size() && p->steps[i].type == Step::TILE && live_tiles_on(); ++i) {
-                Step& t = p->steps[i];
-                uint64_t wm = 0;
-                for (int j = 0; j < TILE_W; ++j) wm |= 1ull << t.tile.wpos[j];
-                if (i == 0) {  // the synthesised pass: the one tile holding x is the grid
-                    t.tile.fix_mask = all & ~wm;
-                    t.tile.fix_val = basis & t.tile.fix_mask;
-                } else {
-                    t.tile.fix_mask = all & ~windowed & ~wm;
-                    t.tile.fix_val = basis & t.tile.fix_mask;
-                    t.tile.zero_mask = wm & ~windowed;
-                    t.tile.zero_val = basis & t.tile.zero_mask;
-                    const int f = __builtin_popcountll(t.tile.fix_mask), z = __builtin_popcountll(t.tile.zero_mask);
-                    t.alg_bytes = s->amp_bytes * (std::ldexp(1.0, s->nl - f - z) + std::ldexp(1.0, s->nl - f));
-                    // each pass reads only amplitudes the previous one wrote: once a
-                    // pass writes every tile, no amplitude is read before it is written
-                    if (!t.tile.fix_mask) p->init_none = true;
-                }
-                windowed |= wm;
-            }
-        }
+        if (first_tile) p->init_none = setup_live_tiles(p->steps, s->nl, s->amp_bytes, basis);
         if (nq > 0) {
             cudaError_t e = cudaMalloc(&p->sim_bins, sizeof(double) << nq);
             if (e != cudaSuccess) {
@@ -1972,6 +2017,8 @@ qj_status qj_debug_tile_sources(int n, int amp_bytes, const qj_gate* gates, int 
     Planner pl;
     pl.auto_fuse_ = !(flags & QJ_FUSE_GATES);
     pl.plan(ctx, gs, true, steps);
+    if (const char* e = getenv("QJ_DEBUG_LIVE"); e && !steps.empty() && steps.front().type == Step::TILE)
+        setup_live_tiles(steps, n, amp_bytes, strtoull(e, nullptr, 0));  // the qj_simulate form from |basis>
     int k = 0;
     for (const Step& st : steps) {
         if (st.type != Step::TILE) continue;
