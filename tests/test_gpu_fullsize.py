@@ -94,6 +94,24 @@ def test_qft30_simulate_every_amplitude(dt):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("dt", [np.complex128, np.complex64], ids=["c128", "c64"])
+@pytest.mark.parametrize("n", [13, 17, 23, 25, 27])
+def test_qft_simulate_every_amplitude_sizes(dt, n):
+    """qj_simulate(QFT n, |x>) at sizes whose live-tile passes give CTAs odd
+    tile counts (paired live tiles: the last pair's second tile is absent) and
+    one or two tiles in all (n = 13); every amplitude against the closed form."""
+    x = (0x2D5A3C9 * n + 777) & ((1 << n) - 1)
+    t = torch.empty(2**n, dtype=TDT[dt], device="cuda")
+    st = qjp.State(t, basis=None)
+    t.fill_(float("nan"))
+    p = st.simulate(x, C.qft(n).gates, qubits=[0, n // 2, n - 1], fuse=True)
+    st.sync()
+    phys = st.layout()
+    worst, _ = qft_check_full(t, n, x, phys)
+    assert worst <= TOL[dt], f"max abs err {worst:.3e}"
+    assert np.max(np.abs(p.cpu().numpy() - 1 / 8)) <= TOL[dt]
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("dt,fuse", [(np.complex128, True), (np.complex64, True), (np.complex128, False)],
                          ids=["c128-fused", "c64-fused", "c128-unfused"])
