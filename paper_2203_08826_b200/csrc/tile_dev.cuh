@@ -615,6 +615,15 @@ __device__ __forceinline__ bool qj_chk(const TileArgs<R>& a, const Cx<R>* p, uin
 // a ring of tile buffers filled by bulk asynchronous copies (TMA engine,
 // cp.async.bulk) that complete on one mbarrier per buffer; a worker
 // synchronises its own 256 threads with a named barrier.
+// Programmatic dependent launch (the JIT kernels are launched with it): let
+// the next pass be scheduled once every CTA of this one is resident, then
+// wait until the previous grid has completed and its writes are visible.
+// Everything before this call touches only host-written tables and SMEM.
+__device__ __forceinline__ void grid_dep_sync() {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void worker_sync(int wk) {
     asm volatile("bar.sync %0, 256;\n" ::"r"(1 + wk) : "memory");
 }
