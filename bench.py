@@ -32,6 +32,7 @@ closed-form check.  Independent per-rank QFT30 replicas are a side field.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -573,7 +574,8 @@ def run_sharded(args, rank, world):
 
     barrier()
     e2e_ms = timed_steps(torch, stream, steps, e2e_step, None)
-    h2d = sum(112 + (4 ** len(gg.targets) * 16 if gg.kind == "dense" else 2 ** len(gg.targets) * 16
+    gsz = ctypes.sizeof(qj.qj.qj_gate)
+    h2d = sum(gsz + (4 ** len(gg.targets) * 16 if gg.kind == "dense" else 2 ** len(gg.targets) * 16
                      if gg.kind == "diag" else 0) for gg in circ.gates)
     # profiled repeat: per-kind device times on this rank (events around every
     # pass / exchange on the state's stream)
@@ -683,7 +685,7 @@ def run_qj(args, rank, world):
     h2d = 0
     gates = wl["circ"].gates
     for g in gates:
-        h2d += 112  # sizeof(qj_gate)
+        h2d += ctypes.sizeof(qj.qj.qj_gate)
         if g.kind in ("dense", "diag", "fsim"):
             cnt = {"dense": 4 ** len(g.targets), "diag": 2 ** len(g.targets), "fsim": 5}[g.kind]
             h2d += cnt * amp_bytes

@@ -9,6 +9,7 @@ is missing, importing this module raises -- there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+from itertools import chain
 import os
 
 import numpy as np
@@ -198,56 +199,55 @@ _GATE_NP = np.dtype({"names": ["kind", "nt", "nc", "targets", "controls", "data"
                      "offsets": [0, 4, 8, 12, 44, 112], "itemsize": 120})
 
 
+def _scatter_rows(field, seqs, lens, ng):
+    """field[i, :lens[i]] = seqs[i] for every row, in one vectorised store."""
+    flat = np.fromiter(chain.from_iterable(seqs), dtype=np.int32)
+    if flat.size:
+        rows = np.repeat(np.arange(ng), lens)
+        starts = np.cumsum(lens) - lens
+        field[rows, np.arange(flat.size) - np.repeat(starts, lens)] = flat
+
+
+def _coeffs(g, k):
+    d = g.data[0]
+    if k == "fsim":
+        return np.append(np.asarray(d).reshape(-1), g.data[1])
+    return d if type(d) is np.ndarray else np.asarray(d)
+
+
 def pack_gates(gates, np_dtype=np.complex128):
     """Marshal gate records (kind/targets/controls/data) into a qj_gate array:
     one numpy record array with the C struct's layout and one contiguous
-    coefficient buffer in the state's dtype.  Returns (qj_gate*, n, keepalive)."""
+    coefficient buffer in the state's dtype.  Returns (qj_gate*, n, keepalive).
+    Vectorised over the gate list (it is on the end-to-end path of every
+    simulate / apply_circuit call that passes Python gates)."""
     assert ctypes.sizeof(qj_gate) == _GATE_NP.itemsize
-    gates = list(gates)
+    gates = gates if isinstance(gates, list) else list(gates)
     ng = len(gates)
     rec = np.zeros(max(1, ng), dtype=_GATE_NP)
-    kinds = [0] * ng
-    nts = [0] * ng
-    ncs = [0] * ng
-    tg = [0] * (MAX_TARGETS * max(1, ng))
-    ct = [0] * (MAX_CONTROLS * max(1, ng))
-    parts, owner, lens = [], [], []
-    ndarray = np.ndarray
-    for i, g in enumerate(gates):
-        t, c = g.targets, g.controls
-        nt, nc = len(t), len(c)
-        if nt > MAX_TARGETS or nc > MAX_CONTROLS:
-            raise QJError(4, f"gate {i}: too many qubits")
-        k = g.kind
-        kinds[i] = KIND[k]
-        nts[i] = nt
-        ncs[i] = nc
-        tg[MAX_TARGETS * i:MAX_TARGETS * i + nt] = t
-        if nc:
-            ct[MAX_CONTROLS * i:MAX_CONTROLS * i + nc] = c
-        if k == "dense" or k == "diag":
-            d = g.data[0]
-            if type(d) is not ndarray:
-                d = np.asarray(d)
-            parts.append(d)
-            owner.append(i)
-            lens.append(d.size)
-        elif k == "fsim":
-            d = np.append(np.asarray(g.data[0]).reshape(-1), g.data[1])
-            parts.append(d)
-            owner.append(i)
-            lens.append(d.size)
+    coeff = None
     if ng:
-        rec["kind"][:ng] = kinds
+        kl = [g.kind for g in gates]
+        tl = [g.targets for g in gates]
+        cl = [g.controls for g in gates]
+        nts = np.fromiter(map(len, tl), dtype=np.int64, count=ng)
+        ncs = np.fromiter(map(len, cl), dtype=np.int64, count=ng)
+        bad = np.nonzero((nts > MAX_TARGETS) | (ncs > MAX_CONTROLS))[0]
+        if bad.size:
+            raise QJError(4, f"gate {int(bad[0])}: too many qubits")
+        rec["kind"][:ng] = [KIND[k] for k in kl]
         rec["nt"][:ng] = nts
         rec["nc"][:ng] = ncs
-        rec["targets"][:ng] = np.asarray(tg, dtype=np.int32).reshape(-1, MAX_TARGETS)[:ng]
-        rec["controls"][:ng] = np.asarray(ct, dtype=np.int32).reshape(-1, MAX_CONTROLS)[:ng]
-    coeff = None
-    if parts:
-        coeff = np.ascontiguousarray(np.concatenate(parts, axis=None).astype(np_dtype, copy=False))
-        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
-        rec["data"][np.asarray(owner)] = np.uint64(coeff.ctypes.data) + offs * np.uint64(coeff.itemsize)
+        _scatter_rows(rec["targets"], tl, nts, ng)
+        if ncs.any():
+            _scatter_rows(rec["controls"], cl, ncs, ng)
+        owner = [i for i, k in enumerate(kl) if k == "dense" or k == "diag" or k == "fsim"]
+        if owner:
+            parts = [_coeffs(gates[i], kl[i]) for i in owner]
+            coeff = np.ascontiguousarray(np.concatenate(parts, axis=None).astype(np_dtype, copy=False))
+            lens = np.fromiter((p.size for p in parts), dtype=np.uint64, count=len(parts))
+            offs = np.cumsum(lens) - lens
+            rec["data"][owner] = np.uint64(coeff.ctypes.data) + offs * np.uint64(coeff.itemsize)
     arr = rec.ctypes.data_as(ctypes.POINTER(qj_gate))
     return arr, ng, (rec, coeff)
 
