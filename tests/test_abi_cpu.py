@@ -228,3 +228,56 @@ def test_host_state_init_validation():
     assert L.qj_state_init_host(ctypes.byref(h), P, 41, 1, 2, K, None) == 5
     assert L.qj_state_init_host(ctypes.byref(h), P, 4, 1, 2, K, None) == 0
     assert L.qj_state_free(h) == 0
+
+
+def _pack_reference(gates, np_dtype):
+    """Gate records built one field at a time from the qj_gate layout in
+    include/qj.h (kind, nt, nc, targets[8], controls[16], data pointer)."""
+    recs, coeffs = [], []
+    for g in gates:
+        r = Q.qj_gate()
+        r.kind = Q.KIND[g.kind]
+        r.nt, r.nc = len(g.targets), len(g.controls)
+        for i, t in enumerate(g.targets):
+            r.targets[i] = t
+        for i, c in enumerate(g.controls):
+            r.controls[i] = c
+        if g.kind in ("dense", "diag"):
+            coeffs.append(np.asarray(g.data[0], dtype=np_dtype).reshape(-1))
+        elif g.kind == "fsim":
+            coeffs.append(np.append(np.asarray(g.data[0]).reshape(-1), g.data[1]).astype(np_dtype))
+        else:
+            coeffs.append(None)
+        recs.append(r)
+    return recs, coeffs
+
+
+@pytest.mark.parametrize("np_dtype", [np.complex128, np.complex64])
+def test_pack_gates_matches_field_by_field(np_dtype):
+    """The vectorised gate-list packing (qj.pack_gates) writes exactly the
+    records and coefficients a field-by-field packing does, for every gate
+    kind, with and without controls, coefficients given as arrays or lists."""
+    from workloads import circuits as C
+    from workloads.gates import Gate
+    rng = np.random.default_rng(5)
+    gates = list(C.random_circuit(12, 300, 3, max_targets=3, max_controls=3).gates)
+    gates += [Gate("i", "dense", (4,), (), (np.eye(2).tolist(),)), Gate("cx", "x", (0,), (1, 2)),
+              Gate("cswap", "swap", (3, 5), (7,)), Gate("d", "diag", (2, 6), (), ([1, 1j, -1, -1j],)),
+              Gate("z", "z", (9,), ())]
+    rng.shuffle(gates)
+    arr, ng, keep = Q.pack_gates(gates, np_dtype)
+    rec, coeff = keep
+    ref, ref_coeffs = _pack_reference(gates, np_dtype)
+    assert ng == len(gates)
+    base = coeff.ctypes.data if coeff is not None else 0
+    item = np.dtype(np_dtype).itemsize
+    for i, (g, r, c) in enumerate(zip(gates, ref, ref_coeffs)):
+        assert arr[i].kind == r.kind and arr[i].nt == r.nt and arr[i].nc == r.nc, i
+        assert list(arr[i].targets) == list(r.targets) and list(arr[i].controls) == list(r.controls), i
+        if c is None:
+            assert rec["data"][i] == 0, i
+        else:
+            off = (int(rec["data"][i]) - base) // item
+            assert np.array_equal(coeff[off:off + c.size], c), i
+    with pytest.raises(Q.QJError):
+        Q.pack_gates([Gate("x", "x", (0,), tuple(range(1, 18)))])
