@@ -208,13 +208,6 @@ def _scatter_rows(field, seqs, lens, ng):
         field[rows, np.arange(flat.size) - np.repeat(starts, lens)] = flat
 
 
-def _coeffs(g, k):
-    d = g.data[0]
-    if k == "fsim":
-        return np.append(np.asarray(d).reshape(-1), g.data[1])
-    return d if type(d) is np.ndarray else np.asarray(d)
-
-
 def pack_gates(gates, np_dtype=np.complex128):
     """Marshal gate records (kind/targets/controls/data) into a qj_gate array:
     one numpy record array with the C struct's layout and one contiguous
@@ -243,11 +236,21 @@ def pack_gates(gates, np_dtype=np.complex128):
             _scatter_rows(rec["controls"], cl, ncs, ng)
         owner = [i for i, k in enumerate(kl) if k == "dense" or k == "diag" or k == "fsim"]
         if owner:
-            parts = [_coeffs(gates[i], kl[i]) for i in owner]
-            coeff = np.ascontiguousarray(np.concatenate(parts, axis=None).astype(np_dtype, copy=False))
-            lens = np.fromiter((p.size for p in parts), dtype=np.uint64, count=len(parts))
+            # coefficients in C order, each gate's block converted to the state's
+            # dtype, joined as bytes (numpy's concatenate costs ~0.3-0.6 us per
+            # small array; thousands of 2x2 blocks are common)
+            dt = np.dtype(np_dtype)
+            parts = [gates[i].data[0] for i in owner]
+            for j, i in enumerate(owner):
+                if kl[i] == "fsim":
+                    parts[j] = np.append(np.asarray(parts[j]).reshape(-1), gates[i].data[1])
+            if {p.dtype if type(p) is np.ndarray else None for p in parts} != {dt}:
+                parts = [np.asarray(p).astype(dt, copy=False) for p in parts]
+            blobs = [p.tobytes() for p in parts]
+            coeff = np.frombuffer(b"".join(blobs), dtype=dt).copy()
+            lens = np.fromiter(map(len, blobs), dtype=np.uint64, count=len(blobs))
             offs = np.cumsum(lens) - lens
-            rec["data"][owner] = np.uint64(coeff.ctypes.data) + offs * np.uint64(coeff.itemsize)
+            rec["data"][owner] = np.uint64(coeff.ctypes.data) + offs
     arr = rec.ctypes.data_as(ctypes.POINTER(qj_gate))
     return arr, ng, (rec, coeff)
 
