@@ -51,6 +51,16 @@ st.sync()
 e, _ = oracle.qft_basis_maxerr(t.cpu().numpy(), n, 77)
 assert e < 1e-12
 print("ok fused qft16", e, flush=True)
+# live-tile simulate with paired tiles (n = 25: several tiles per CTA, odd counts)
+for n, dtp, tol in ((25, torch.complex128, 1e-12), (25, torch.complex64, 1e-5)):
+    t = torch.empty(2**n, dtype=dtp, device=dev)
+    st = qj.State(t, basis=None, stream=torch.cuda.Stream())
+    st.simulate(4242, C.qft(n).gates, qubits=[0, 1, 2])
+    st.sync()
+    e, _ = oracle.qft_basis_maxerr(t.cpu().numpy().astype(np.complex128), n, 4242, phys=st.layout())
+    assert e < tol, e
+    print("ok simulate qft25", dtp, e, flush=True)
+    del st, t
 # ring form (TMA): needs >= 148 tiles -> n = 20 c128
 n = 20
 t = torch.empty(2**n, dtype=torch.complex128, device=dev)
