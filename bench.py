@@ -801,7 +801,12 @@ def run_qj(args, rank, world):
         "paper_fusion": paper,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_ms / 1e3 / (steps * world), "unit": "s/circuit",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "inputs": "every step: the Python gate list packed into qj_gate records + coefficients "
+                          "(h2d_bytes_per_step) and passed with the basis index through the C ABI; the library "
+                          "compares every record and coefficient with its cached plan's key and, when equal, "
+                          "replays the plan whose device tables hold those same values (a changed gate list "
+                          "re-plans and uploads); the marginal is copied to pinned host memory and synchronised"},
         "gpu_launches": m["ctr"]["launches"],
         "clocks": m["clk"].summary(),
         "dry_run_s": m["dry"], "lib_load_s": load_s,
